@@ -1,0 +1,191 @@
+/*
+ * tlb.h -- C ABI of the B200-native D2Q37 thermal lattice-Boltzmann step
+ * (libtlb.so, built from paper_1703_00185_b200/csrc/).
+ *
+ * The reference (`thermolb`, /root/reference/pkg/src/thermolb) has no FFI:
+ * its hot path is plain Python functions.  Each entry point below replaces
+ * one of them; the Python mirror (paper_1703_00185_b200/kernels.py,
+ * runtime.py) keeps the reference signatures and calls these through ctypes.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  Field memory is owned by the caller
+ *    (torch tensors on the host side); the library never allocates fields.
+ *  - A field is a strided (Q=37, NX, NY) view: element (l, x, y) lives at
+ *    base[l*sl + x*sx + y*sy] (the reference's canonical view,
+ *    geometry.py:95-100; SoA canonical strides are (NX*NY, NY, 1),
+ *    geometry.py:72-73).  Coordinates are padded (halo-inclusive).
+ *  - Regions are half-open [x0,x1) x [y0,y1) in padded coordinates and must
+ *    lie inside the physical region (kernels.py:149-156) or the call returns
+ *    TLB_ERR_CONTRACT.  An empty region is a no-op (kernels.py:221-222).
+ *  - All compute calls are stream-ordered and asynchronous.  Per-site
+ *    failures (non-positive density, T_bar <= 0, bad wall state) are written
+ *    to a caller-owned device status block (TlbStatus) and surface when the
+ *    host reads it; the host layer raises the errors.py exception.
+ *  - Return value: 0 = ok, else a TLB_ERR_* code; message via
+ *    tlb_last_error().
+ */
+#ifndef TLB_H
+#define TLB_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st *tlb_stream_t; /* == cudaStream_t */
+
+#define TLB_Q 37
+#define TLB_WALL_ROWS 3 /* kernels.py:18 */
+
+/* return codes */
+#define TLB_OK 0
+#define TLB_ERR_CONTRACT 1    /* ContractViolation (bad region/index)      */
+#define TLB_ERR_CUDA 2        /* CUDA runtime error                        */
+#define TLB_ERR_STENCIL 3     /* stencil not set / not the D2Q37 ordering  */
+#define TLB_ERR_UNSUPPORTED 4 /* UnsupportedCaseError                      */
+#define TLB_ERR_DOMAIN 5      /* DomainError detected on the host          */
+
+/* device status bits (TlbStatus.flags), checked by the host */
+#define TLB_ST_DEGENERATE 1u /* rho <= 0 (or NaN) in moments  kernels.py:62-66  */
+#define TLB_ST_SHIFT 2u      /* T_bar <= 0 in apply_shift     kernels.py:134-135 */
+#define TLB_ST_EQ_DOMAIN 4u  /* rho<=0 or T<=0, checked eq.   kernels.py:85-86   */
+
+/* field view */
+typedef struct TlbField {
+    double *base;           /* element (0, 0, 0)                            */
+    int64_t sl, sx, sy;     /* strides (elements) of l, x, y                */
+    int32_t Lx, Ly, Hx, Hy; /* physical extents and halo widths             */
+} TlbField;
+
+/* physics (kernels.py:21-38); D is fixed to 2 */
+typedef struct TlbParams {
+    double tau, gx, gy, dt;
+    double Twall_top, Twall_bot;
+    int32_t order; /* Hermite order 2, 3 or 4 (4 = D2Q37 default)          */
+    int32_t arith; /* TLB_ARITH_EXACT (bitwise = reference) or _FAST       */
+} TlbParams;
+
+#define TLB_ARITH_EXACT 0
+#define TLB_ARITH_FAST 1
+
+typedef struct TlbRegion {
+    int32_t x0, x1, y0, y1;
+} TlbRegion;
+
+/* caller-owned DEVICE memory, zero-initialised by the caller */
+typedef struct TlbStatus {
+    uint32_t flags;          /* OR of TLB_ST_* bits                          */
+    int32_t site_x[3];       /* first (by atomic race) failing site per bit  */
+    int32_t site_y[3];
+    int32_t step;            /* step tag of the first failure (-1 unknown)   */
+    uint32_t pad;
+    unsigned long long negatives; /* count of f<0 written (count_negative) */
+} TlbStatus;
+
+/* step flags for tlb_fused / tlb_step */
+#define TLB_F_WALL_BOT 1   /* bc rows [Hy, Hy+3) at Twall_bot before collide  */
+#define TLB_F_WALL_TOP 2   /* bc rows [Hy+Ly-3, Hy+Ly) at Twall_top            */
+#define TLB_F_CLAMP_Y 4    /* read Y halo as the wall-row extension (runtime.py:296-305) */
+#define TLB_F_WRAP_X 8     /* read X halo periodically (self ring, Np = 1)     */
+#define TLB_F_WRAP_Y 16    /* read Y halo periodically (periodic_y)            */
+#define TLB_F_COUNT_NEG 32 /* add count of written f<0 to status->negatives    */
+
+/* library */
+int tlb_version(void);
+const char *tlb_last_error(void);
+int tlb_set_device(int device);
+int tlb_device_count(void);
+
+/* Upload the stencil constants to `device`.  c is (37,2) int64 in the
+ * reference ordering (velocity_set.py:55-59), w (37,) the weights, cs2 the
+ * squared sound speed -- all as built by velocity_set.build_velocity_set
+ * (velocity_set.py:128-130).  ex = c/cs and q = ex^2+ey^2 are derived here
+ * with the expressions of kernels.py:87-97.  Returns TLB_ERR_STENCIL if c is
+ * not the D2Q37 ordering or w is not constant per speed shell. */
+int tlb_set_stencil(int device, const int64_t *c, const double *w, double cs2);
+
+/* propagate (pull)      replaces kernels.propagate, kernels.py:168-177 */
+int tlb_propagate(const TlbField *prv, const TlbField *nxt, TlbRegion r,
+                  tlb_stream_t stream);
+
+/* bc (wall rows)        replaces kernels.bc, kernels.py:180-203.
+ * Columns [x0, x1); top/bottom select the walls. */
+int tlb_bc(const TlbField *f, const TlbParams *p, int top, int bottom,
+           int32_t x0, int32_t x1, TlbStatus *status, tlb_stream_t stream);
+
+/* collide (in place allowed: in == out)   replaces kernels.collide,
+ * kernels.py:139-146, on the region of a field (runtime.py:322-324) or on a
+ * (Q, nx, ny) block described as a halo-free field. */
+int tlb_collide(const TlbField *in, const TlbField *out, TlbRegion r,
+                const TlbParams *p, int flags, TlbStatus *status,
+                tlb_stream_t stream);
+
+/* fused propagate(+bc)+collide   replaces kernels.propagate_collide_fused,
+ * kernels.py:206-224, extended with bc on wall rows (RankWorker._tb_frame,
+ * runtime.py:340-353) so one launch is a full staged step on its region. */
+int tlb_fused(const TlbField *prv, const TlbField *nxt, TlbRegion r,
+              const TlbParams *p, int flags, TlbStatus *status,
+              tlb_stream_t stream);
+
+/* One whole time step of a rank whose X ring neighbours are itself
+ * (Np = 1) and whose Y direction has walls or is periodic: a single fused
+ * launch over the physical region with implicit halos (WRAP_X + CLAMP_Y or
+ * WRAP_Y).  Bitwise equal to RankWorker.step (runtime.py:355-400). */
+int tlb_step_self(const TlbField *prv, const TlbField *nxt,
+                  const TlbParams *p, int walls, int periodic_y,
+                  int count_neg, TlbStatus *status, tlb_stream_t stream);
+
+/* moments               replaces kernels.moments, kernels.py:41-71.
+ * Outputs are (nx, ny) arrays with row stride ld (elements). */
+int tlb_moments(const TlbField *f, TlbRegion r, double *rho, double *ux,
+                double *uy, double *T, int64_t ld, int check,
+                TlbStatus *status, tlb_stream_t stream);
+
+/* equilibrium           replaces kernels.equilibrium, kernels.py:74-125,
+ * on n sites; out is (37, n) with leading dimension ld. */
+int tlb_equilibrium(const double *rho, const double *ux, const double *uy,
+                    const double *T, int64_t n, int order, int arith,
+                    double *out, int64_t ld, int check, TlbStatus *status,
+                    tlb_stream_t stream);
+
+/* apply_shift           replaces kernels.apply_shift, kernels.py:128-136 */
+int tlb_apply_shift(const double *ux, const double *uy, const double *T,
+                    int64_t n, const TlbParams *p, double *ub, double *vb,
+                    double *Tb, TlbStatus *status, tlb_stream_t stream);
+
+/* count_negative        replaces kernels.count_negative, kernels.py:227-229 */
+int tlb_count_negative(const TlbField *f, TlbRegion r, TlbStatus *status,
+                       tlb_stream_t stream);
+
+/* _extend_wall_halos    replaces RankWorker._extend_wall_halos,
+ * runtime.py:296-305 (all x, all 37 populations). */
+int tlb_extend_walls(const TlbField *f, int upper, int lower,
+                     tlb_stream_t stream);
+
+/* Face-plan X payloads  replace RankWorker.pack_x / unpack_x,
+ * runtime.py:199-224 (plans runtime.py:94-107): for d = 1..3, for l with
+ * sign*c_l,x >= d in ascending l, one full-height column of NY values.
+ * ymode selects how Y-halo rows are sourced when packing: 0 = memory as is
+ * (the reference), 1 = wall extension (clamp), 2 = periodic wrap. */
+int64_t tlb_face_payload_len(const TlbField *f); /* 26 * NY */
+int tlb_pack_x(const TlbField *f, int sign, int ymode, double *buf,
+               tlb_stream_t stream);
+int tlb_unpack_x(const TlbField *f, int sign, const double *buf,
+                 tlb_stream_t stream);
+
+/* pbc_c / pbc_nc with the rank as its own neighbour (1-D ring of one rank;
+ * periodic Y): runtime.py:248-284. */
+int tlb_pbc_self_x(const TlbField *f, tlb_stream_t stream);
+int tlb_pbc_self_y(const TlbField *f, tlb_stream_t stream);
+
+/* Fill a field's X halo columns (face-plan populations, all NY rows) from
+ * peer fields: left neighbour's right edge -> low-x halo, right neighbour's
+ * left edge -> high-x halo.  Pointers may be peer-mapped (NVLink). */
+int tlb_halo_from_peers(const TlbField *f, const TlbField *left,
+                        const TlbField *right, tlb_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TLB_H */

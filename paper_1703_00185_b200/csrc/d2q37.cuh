@@ -1,0 +1,463 @@
+// d2q37.cuh -- per-site D2Q37 arithmetic for sm_100a.
+//
+// Two variants of the reference collide (kernels.py:139-146):
+//
+//  * Exact: the reference's numpy expression tree (kernels.py:41-136,
+//    SURVEY Appendix B) with one IEEE binary64 operation per reference
+//    operation, spelled with __dadd_rn/__dmul_rn so nvcc cannot contract or
+//    reorder.  FMA is used ONLY where the product is exact (multiplier a power
+//    of two), where fma(a,b,c) == RN(c + a*b) bit for bit.  Results are
+//    bitwise equal to the reference.  Three restructurings keep the bits
+//    while cutting work:
+//      - speed-shell CSE: every sub-expression that depends only on (site, q)
+//        (theta*q, 3*theta*q, ...) is evaluated once per shell, not per l;
+//      - +/-c pairing: for c_l' = -c_l, p' = -p exactly, so p^2, c2 and c4
+//        are identical and c3 flips sign exactly; one evaluation serves both;
+//      - division by 6 and 24 uses Markstein's correction
+//        q = RN(x*RN(1/b)); r = fma(-q,b,x); RN(q + r*RN(1/b)) == RN(x/b)
+//        (q is within 1 ulp of x/b for b = 6*2^k, so the theorem applies);
+//        division by cs and cs2 uses two correction steps.
+//  * Fast: FMA everywhere, the Hermite polynomial rewritten per shell as a
+//    degree-4 polynomial in p with site-dependent coefficients, even/odd split
+//    over +/-c pairs.  Agrees with the reference to ~1e-15 relative per step.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace tlb {
+
+constexpr int Q = 37;
+constexpr int NSHELL = 8;
+
+// Reference ordering velocity_set.py:46-59.
+__host__ __device__ constexpr int CX(int l) {
+    constexpr int t[Q] = {0, -1, 0, 0, 1, -1, -1, 1, 1, -2, 0, 0, 2,
+                          -2, -2, -1, -1, 1, 1, 2, 2, -2, -2, 2, 2,
+                          -3, 0, 0, 3, -3, -3, -1, -1, 1, 1, 3, 3};
+    return t[l];
+}
+__host__ __device__ constexpr int CY(int l) {
+    constexpr int t[Q] = {0, 0, -1, 1, 0, -1, 1, -1, 1, 0, -2, 2, 0,
+                          -1, 1, -2, 2, -2, 2, -1, 1, -2, 2, -2, 2,
+                          0, -3, 3, 0, -1, 1, -3, 3, -3, 3, -1, 1};
+    return t[l];
+}
+// speed shells (0,0) (1,0) (1,1) (2,0) (2,1) (2,2) (3,0) (3,1): [start, n)
+__host__ __device__ constexpr int SH_START(int s) {
+    constexpr int t[NSHELL] = {0, 1, 5, 9, 13, 21, 25, 29};
+    return t[s];
+}
+__host__ __device__ constexpr int SH_N(int s) {
+    constexpr int t[NSHELL] = {1, 4, 4, 4, 8, 4, 4, 8};
+    return t[s];
+}
+__host__ __device__ constexpr int SHELL_OF(int l) {
+    return l < 1 ? 0 : l < 5 ? 1 : l < 9 ? 2 : l < 13 ? 3 : l < 21 ? 4
+         : l < 25 ? 5 : l < 29 ? 6 : 7;
+}
+// Within a shell the signed permutations are sorted, so the partner -c of
+// entry i is entry n-1-i.
+__host__ __device__ constexpr int PARTNER(int l) {
+    return 2 * SH_START(SHELL_OF(l)) + SH_N(SHELL_OF(l)) - 1 - l;
+}
+__host__ __device__ constexpr int iabs(int v) { return v < 0 ? -v : v; }
+__host__ __device__ constexpr bool pow2(int v) {
+    return v == 1 || v == 2 || v == 4 || v == 8;
+}
+
+// Stencil constants, uploaded once per device (tlb_set_stencil).
+struct StencilConst {
+    double E[4];       // |c|/cs for |c| = 0..3 (kernels.py:95-96)
+    double qsh[NSHELL]; // q = ex^2 + ey^2 per shell (kernels.py:97)
+    double wsh[NSHELL]; // w per shell (velocity_set.py:108)
+    double cs, cs2, rcs, rcs2; // sqrt(cs2), cs2 and RN reciprocals
+    double r6, r24;            // RN(1/6), RN(1/24)
+    int set;
+};
+
+// Physics constants derived on the host exactly as the reference does.
+struct Phys {
+    double K1, K2, K3;  // tau*gx, tau*gy, tau*tau*g2/D  (kernels.py:130-133)
+    double omega;       // dt/tau                        (kernels.py:145)
+    double Tbot, Ttop;  // wall temperatures
+    int order;
+};
+
+// Defined here: the library is a single translation unit (no -rdc).
+__constant__ StencilConst C;
+
+// ---------------------------------------------------------------- exact --
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double dfma(double a, double b, double c) { return __fma_rn(a, b, c); }
+
+// acc + c*f with the reference's rounding: exact product -> fma is identical.
+template <int c>
+__device__ __forceinline__ double acc_cf(double acc, double f) {
+    if constexpr (c == 0) {
+        return acc;
+    } else if constexpr (pow2(iabs(c))) {
+        return dfma((double)c, f, acc);
+    } else {
+        return dadd(acc, dmul((double)c, f));
+    }
+}
+
+// RN(x / b) for the constant b with RN(1/b) = y (two Markstein steps).
+__device__ __forceinline__ double div_const2(double x, double b, double y) {
+    double q0 = dmul(x, y);
+    double r0 = dfma(-q0, b, x);
+    double q1 = dfma(r0, y, q0);
+    double r1 = dfma(-q1, b, x);
+    return dfma(r1, y, q1);
+}
+// RN(x / b), b in {6, 24}: one Markstein step suffices (see header).
+__device__ __forceinline__ double div_const1(double x, double b, double y) {
+    double q0 = dmul(x, y);
+    double r0 = dfma(-q0, b, x);
+    return dfma(r0, y, q0);
+}
+
+template <int l>
+__device__ __forceinline__ double pdot_exact(double vx, double vy) {
+    // p = ex*vx + ey*vy (kernels.py:98).  A zero component contributes a
+    // signed zero, which cannot change a non-zero sum; it is dropped.
+    constexpr int cx = CX(l), cy = CY(l);
+    if constexpr (cx == 0 && cy == 0) {
+        return 0.0;
+    } else if constexpr (cx == 0) {
+        return dmul(cy > 0 ? C.E[iabs(cy)] : -C.E[iabs(cy)], vy);
+    } else if constexpr (cy == 0) {
+        return dmul(cx > 0 ? C.E[iabs(cx)] : -C.E[iabs(cx)], vx);
+    } else {
+        return dadd(dmul(cx > 0 ? C.E[iabs(cx)] : -C.E[iabs(cx)], vx),
+                    dmul(cy > 0 ? C.E[iabs(cy)] : -C.E[iabs(cy)], vy));
+    }
+}
+
+// Site-level quantities of equilibrium() (kernels.py:87-91, 100-121).
+struct EqSite {
+    double rho, vx, vy, theta, s;
+    double s2t, s4t, t3, t6, t3t, tt4, c3x;
+};
+
+__device__ __forceinline__ EqSite eq_site_exact(double rho, double ux, double uy,
+                                                double T) {
+    EqSite e;
+    e.rho = rho;
+    e.vx = div_const2(ux, C.cs, C.rcs);
+    e.vy = div_const2(uy, C.cs, C.rcs);
+    e.theta = dsub(div_const2(T, C.cs2, C.rcs2), 1.0);
+    e.s = dadd(dmul(e.vx, e.vx), dmul(e.vy, e.vy));
+    const double th = e.theta;
+    e.s2t = dadd(e.s, dmul(2.0, th));          // s + D*theta
+    e.s4t = dadd(e.s, dmul(4.0, th));          // s + (D+2)*theta
+    e.t3 = dmul(3.0, th);                      // 3.0*theta
+    e.t6 = dmul(6.0, th);                      // 6.0*theta
+    e.t3t = dmul(e.t3, th);                    // 3.0*theta*theta
+    e.tt4 = dmul(dmul(th, th), 4.0);           // theta*theta*(D+2)
+    const double t8 = dmul(8.0, th);           // (2D+4)*theta == D(D+2)*theta
+    const double inner3 = dadd(dadd(dmul(e.s, e.s), dmul(t8, e.s)), dmul(t8, th));
+    e.c3x = dmul(3.0, inner3);
+    return e;
+}
+
+// Per-shell sub-expressions (depend on q only).
+struct EqShell {
+    double tq, t3q, t6q, t3tqq, qs, tt4q, wr;
+};
+
+template <int sh>
+__device__ __forceinline__ EqShell eq_shell_exact(const EqSite &e) {
+    const double q = C.qsh[sh];
+    EqShell z;
+    z.tq = dmul(e.theta, q);
+    z.t3q = dmul(e.t3, q);
+    z.t6q = dmul(e.t6, q);
+    z.t3tqq = dmul(dmul(e.t3t, q), q);
+    z.qs = dmul(q, e.s);
+    z.tt4q = dmul(e.tt4, q);
+    z.wr = dmul(C.wsh[sh], e.rho);             // w*rho
+    return z;
+}
+
+// Equilibrium pair (feq for +c and -c) with the reference rounding.
+template <int ORDER>
+__device__ __forceinline__ void eq_pair_exact(const EqSite &e, const EqShell &z,
+                                              double p, double &fp, double &fm) {
+    const double pp = dmul(p, p);
+    const double c2 = dsub(dadd(pp, z.tq), e.s2t);
+    double bp = dfma(0.5, c2, dadd(1.0, p));   // (1+p) + 0.5*c2
+    double bm = dfma(0.5, c2, dsub(1.0, p));
+    if constexpr (ORDER >= 3) {
+        const double ppp = dmul(pp, p);
+        const double c3 = dsub(dadd(ppp, dmul(z.t3q, p)), dmul(dmul(3.0, p), e.s4t));
+        const double d6 = div_const1(c3, 6.0, C.r6);
+        bp = dadd(bp, d6);
+        bm = dsub(bm, d6);
+        if constexpr (ORDER >= 4) {
+            const double pppp = dmul(ppp, p);
+            const double B = dmul(dmul(z.t6q, p), p);
+            const double sum1 = dadd(dadd(pppp, B), z.t3tqq);
+            const double in6 = dadd(dadd(dmul(dmul(e.s, p), p),
+                                         dmul(e.theta, dadd(dmul(dmul(6.0, p), p), z.qs))),
+                                    z.tt4q);
+            const double c4 = dadd(dsub(sum1, dmul(6.0, in6)), e.c3x);
+            const double d24 = div_const1(c4, 24.0, C.r24);
+            bp = dadd(bp, d24);
+            bm = dadd(bm, d24);
+        }
+    }
+    fp = dmul(z.wr, bp);
+    fm = dmul(z.wr, bm);
+}
+
+// Rest population l = 0 (p == 0 exactly up to the sign of zero).
+template <int ORDER>
+__device__ __forceinline__ double eq_rest_exact(const EqSite &e, const EqShell &z) {
+    double fp, fm;
+    eq_pair_exact<ORDER>(e, z, 0.0, fp, fm);
+    return fp;
+}
+
+// out = f - omega*(f - feq)  (kernels.py:146)
+__device__ __forceinline__ double relax_exact(double f, double feq, double omega) {
+    return dsub(f, dmul(omega, dsub(f, feq)));
+}
+
+// MODE 0: f <- equilibrium (bc);  MODE 1: f <- BGK relax toward equilibrium
+template <int ORDER, int MODE, int sh>
+__device__ __forceinline__ void eq_shell_apply_exact(double (&f)[Q], const EqSite &e,
+                                                     double omega) {
+    const EqShell z = eq_shell_exact<sh>(e);
+    constexpr int s0 = SH_START(sh), n = SH_N(sh);
+    if constexpr (sh == 0) {
+        const double feq = eq_rest_exact<ORDER>(e, z);
+        f[0] = MODE ? relax_exact(f[0], feq, omega) : feq;
+    } else {
+#pragma unroll
+        for (int i = 0; i < n / 2; ++i) {
+            const int l = s0 + i;  // partner s0 + n - 1 - i
+            double p;
+            // dispatch the compile-time pdot through a switch on l
+            switch (l) {
+#define TLB_PD(L) case L: p = pdot_exact<L>(e.vx, e.vy); break;
+                TLB_PD(1) TLB_PD(2) TLB_PD(5) TLB_PD(6) TLB_PD(9) TLB_PD(10)
+                TLB_PD(13) TLB_PD(14) TLB_PD(15) TLB_PD(16) TLB_PD(21) TLB_PD(22)
+                TLB_PD(25) TLB_PD(26) TLB_PD(29) TLB_PD(30) TLB_PD(31) TLB_PD(32)
+#undef TLB_PD
+                default: p = 0.0;
+            }
+            double fp, fm;
+            eq_pair_exact<ORDER>(e, z, p, fp, fm);
+            const int lm = s0 + n - 1 - i;
+            f[l] = MODE ? relax_exact(f[l], fp, omega) : fp;
+            f[lm] = MODE ? relax_exact(f[lm], fm, omega) : fm;
+        }
+    }
+}
+
+template <int ORDER, int MODE>
+__device__ __forceinline__ void eq_all_exact(double (&f)[Q], const EqSite &e, double omega) {
+    eq_shell_apply_exact<ORDER, MODE, 0>(f, e, omega);
+    eq_shell_apply_exact<ORDER, MODE, 1>(f, e, omega);
+    eq_shell_apply_exact<ORDER, MODE, 2>(f, e, omega);
+    eq_shell_apply_exact<ORDER, MODE, 3>(f, e, omega);
+    eq_shell_apply_exact<ORDER, MODE, 4>(f, e, omega);
+    eq_shell_apply_exact<ORDER, MODE, 5>(f, e, omega);
+    eq_shell_apply_exact<ORDER, MODE, 6>(f, e, omega);
+    eq_shell_apply_exact<ORDER, MODE, 7>(f, e, omega);
+}
+
+// rho = sum_l f_l in fixed l order from +0.0 (kernels.py:49, 54; bc :198-200)
+__device__ __forceinline__ double rho_exact(const double (&f)[Q]) {
+    double rho = 0.0;
+#pragma unroll
+    for (int l = 0; l < Q; ++l) rho = dadd(rho, f[l]);
+    return rho;
+}
+
+template <int l>
+__device__ __forceinline__ void mom_step(const double (&f)[Q], double &rho, double &mx,
+                                         double &my, double &e2) {
+    constexpr int cx = CX(l), cy = CY(l), c2 = cx * cx + cy * cy;
+    rho = dadd(rho, f[l]);
+    mx = acc_cf<cx>(mx, f[l]);
+    my = acc_cf<cy>(my, f[l]);
+    e2 = acc_cf<c2>(e2, f[l]);
+}
+
+template <int... Ls>
+struct MomSeq {
+    __device__ __forceinline__ static void run(const double (&f)[Q], double &rho,
+                                               double &mx, double &my, double &e2) {
+        (mom_step<Ls>(f, rho, mx, my, e2), ...);
+    }
+};
+
+// moments (kernels.py:41-71).  Returns false if !(rho > 0).
+__device__ __forceinline__ bool moments_exact(const double (&f)[Q], double &rho, double &ux,
+                                              double &uy, double &T) {
+    double r = 0.0, mx = 0.0, my = 0.0, e2 = 0.0;
+    MomSeq<0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16, 17, 18, 19, 20,
+           21, 22, 23, 24, 25, 26, 27, 28, 29, 30, 31, 32, 33, 34, 35, 36>::run(f, r, mx, my, e2);
+    rho = r;
+    ux = __ddiv_rn(mx, r);
+    uy = __ddiv_rn(my, r);
+    T = __ddiv_rn(dsub(e2, dmul(r, dadd(dmul(ux, ux), dmul(uy, uy)))), dmul(2.0, r));
+    return r > 0.0;
+}
+
+// collide one site in place (kernels.py:139-146).  Returns TLB_ST_* bits.
+template <int ORDER>
+__device__ __forceinline__ unsigned collide_exact(double (&f)[Q], const Phys &P) {
+    double rho, ux, uy, T;
+    if (!moments_exact(f, rho, ux, uy, T)) return 1u;
+    const double ub = dadd(ux, P.K1);
+    const double vb = dadd(uy, P.K2);
+    const double Tb = dsub(T, P.K3);
+    if (!(Tb > 0.0)) return 2u;
+    const EqSite e = eq_site_exact(rho, ub, vb, Tb);
+    eq_all_exact<ORDER, 1>(f, e, P.omega);
+    return 0u;
+}
+
+// bc on one wall site (kernels.py:197-203): rho = sum f, f = feq(rho,0,0,Tw).
+template <int ORDER>
+__device__ __forceinline__ unsigned bc_exact(double (&f)[Q], double Tw) {
+    const double rho = rho_exact(f);
+    const EqSite e = eq_site_exact(rho, 0.0, 0.0, Tw);
+    eq_all_exact<ORDER, 0>(f, e, 0.0);
+    return (rho > 0.0) ? 0u : 4u;
+}
+
+// ----------------------------------------------------------------- fast --
+template <int l>
+__device__ __forceinline__ double pdot_fast(double vx, double vy) {
+    constexpr int cx = CX(l), cy = CY(l);
+    if constexpr (cx == 0 && cy == 0) {
+        return 0.0;
+    } else if constexpr (cx == 0) {
+        return (cy > 0 ? C.E[iabs(cy)] : -C.E[iabs(cy)]) * vy;
+    } else if constexpr (cy == 0) {
+        return (cx > 0 ? C.E[iabs(cx)] : -C.E[iabs(cx)]) * vx;
+    } else {
+        return fma(cx > 0 ? C.E[iabs(cx)] : -C.E[iabs(cx)], vx,
+                   (cy > 0 ? C.E[iabs(cy)] : -C.E[iabs(cy)]) * vy);
+    }
+}
+
+struct FastSite {
+    double theta, s, vx, vy, W; // W = omega*rho (relax) or rho (bc)
+};
+
+// Hermite polynomial of kernels.py:99-123 regrouped in powers of p:
+// poly = A0 + A1 p + A2 p^2 + A3 p^3 + A4 p^4 with a = theta*q - s:
+// A0 = 1 + (a-2th)/2 + [a^2/8 - th*a + th^2]_{order 4}, A1 = 1 + [(a-4th)/2]_{>=3},
+// A2 = 1/2 + [(a-6th)/4]_{4}, A3 = [1/6]_{>=3}, A4 = [1/24]_{4}.
+template <int ORDER, int MODE, int sh>
+__device__ __forceinline__ void fast_shell(double (&f)[Q], const FastSite &e, double omr) {
+    const double q = C.qsh[sh];
+    const double th = e.theta;
+    const double a = fma(th, q, -e.s);
+    const double W = e.W * C.wsh[sh];
+    double A0 = fma(0.5, a - 2.0 * th, 1.0);
+    double A1 = 1.0, A2 = 0.5, A3 = 0.0, A4 = 0.0;
+    if constexpr (ORDER >= 3) {
+        A1 = fma(0.5, a - 4.0 * th, 1.0);
+        A3 = 1.0 / 6.0;
+    }
+    if constexpr (ORDER >= 4) {
+        A0 += fma(0.125 * a, a, th * (th - a));
+        A2 = fma(0.25, a - 6.0 * th, 0.5);
+        A4 = 1.0 / 24.0;
+    }
+    A0 *= W; A1 *= W; A2 *= W; A3 *= W; A4 *= W;
+    constexpr int s0 = SH_START(sh), n = SH_N(sh);
+    if constexpr (sh == 0) {
+        f[0] = MODE ? fma(omr, f[0], A0) : A0;
+    } else {
+#pragma unroll
+        for (int i = 0; i < n / 2; ++i) {
+            const int l = s0 + i, lm = s0 + n - 1 - i;
+            double p;
+            switch (l) {
+#define TLB_PD(L) case L: p = pdot_fast<L>(e.vx, e.vy); break;
+                TLB_PD(1) TLB_PD(2) TLB_PD(5) TLB_PD(6) TLB_PD(9) TLB_PD(10)
+                TLB_PD(13) TLB_PD(14) TLB_PD(15) TLB_PD(16) TLB_PD(21) TLB_PD(22)
+                TLB_PD(25) TLB_PD(26) TLB_PD(29) TLB_PD(30) TLB_PD(31) TLB_PD(32)
+#undef TLB_PD
+                default: p = 0.0;
+            }
+            const double p2 = p * p;
+            const double ev = fma(p2, fma(p2, A4, A2), A0);
+            const double od = p * fma(p2, A3, A1);
+            if (MODE) {
+                f[l] = fma(omr, f[l], ev + od);
+                f[lm] = fma(omr, f[lm], ev - od);
+            } else {
+                f[l] = ev + od;
+                f[lm] = ev - od;
+            }
+        }
+    }
+}
+
+template <int ORDER, int MODE>
+__device__ __forceinline__ void fast_all(double (&f)[Q], const FastSite &e, double omr) {
+    fast_shell<ORDER, MODE, 0>(f, e, omr);
+    fast_shell<ORDER, MODE, 1>(f, e, omr);
+    fast_shell<ORDER, MODE, 2>(f, e, omr);
+    fast_shell<ORDER, MODE, 3>(f, e, omr);
+    fast_shell<ORDER, MODE, 4>(f, e, omr);
+    fast_shell<ORDER, MODE, 5>(f, e, omr);
+    fast_shell<ORDER, MODE, 6>(f, e, omr);
+    fast_shell<ORDER, MODE, 7>(f, e, omr);
+}
+
+template <int ORDER>
+__device__ __forceinline__ unsigned collide_fast(double (&f)[Q], const Phys &P) {
+    double r0 = 0.0, r1 = 0.0, mx = 0.0, my = 0.0, e2 = 0.0;
+#pragma unroll
+    for (int l = 0; l < Q; ++l) {
+        if (l & 1) r1 += f[l]; else r0 += f[l];
+        if (CX(l)) mx = fma((double)CX(l), f[l], mx);
+        if (CY(l)) my = fma((double)CY(l), f[l], my);
+        if (CX(l) * CX(l) + CY(l) * CY(l))
+            e2 = fma((double)(CX(l) * CX(l) + CY(l) * CY(l)), f[l], e2);
+    }
+    const double rho = r0 + r1;
+    if (!(rho > 0.0)) return 1u;
+    const double ri = 1.0 / rho;
+    const double ux = mx * ri, uy = my * ri;
+    const double T = 0.5 * ri * fma(-rho, fma(ux, ux, uy * uy), e2);
+    FastSite e;
+    e.vx = (ux + P.K1) * C.rcs;
+    e.vy = (uy + P.K2) * C.rcs;
+    const double Tb = T - P.K3;
+    if (!(Tb > 0.0)) return 2u;
+    e.theta = fma(Tb, C.rcs2, -1.0);
+    e.s = fma(e.vx, e.vx, e.vy * e.vy);
+    e.W = P.omega * rho;
+    fast_all<ORDER, 1>(f, e, 1.0 - P.omega);
+    return 0u;
+}
+
+template <int ORDER>
+__device__ __forceinline__ unsigned bc_fast(double (&f)[Q], double Tw) {
+    double r0 = 0.0, r1 = 0.0;
+#pragma unroll
+    for (int l = 0; l < Q; ++l) {
+        if (l & 1) r1 += f[l]; else r0 += f[l];
+    }
+    const double rho = r0 + r1;
+    FastSite e;
+    e.vx = 0.0; e.vy = 0.0; e.s = 0.0;
+    e.theta = fma(Tw, C.rcs2, -1.0);
+    e.W = rho;
+    fast_all<ORDER, 0>(f, e, 0.0);
+    return (rho > 0.0) ? 0u : 4u;
+}
+
+}  // namespace tlb

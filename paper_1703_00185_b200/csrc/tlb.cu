@@ -1,0 +1,741 @@
+// tlb.cu -- sm_100a kernels and the C ABI of include/tlb.h.
+//
+// Data layout: SoA FP64, y contiguous.  One thread owns one
+// lattice site and keeps its 37 populations in registers: it issues all 37
+// (shifted, coalesced-along-y) loads up front, runs bc/collide in registers
+// and issues 37 coalesced stores -- 592 B of HBM traffic per site, the
+// algorithmic minimum for a pull step.  There is no GEMM-shaped work here,
+// so no tensor cores; the arithmetic runs on the FP64 pipe (DFMA/DMUL/DADD).
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <cmath>
+#include <mutex>
+#include <string>
+
+#include "../../include/tlb.h"
+#include "d2q37.cuh"
+
+using namespace tlb;
+
+// ------------------------------------------------------------ error state --
+static thread_local std::string g_msg;
+
+static int fail(int code, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_msg = buf;
+    return code;
+}
+
+#define TLB_CUDA_CHECK(expr)                                                  \
+    do {                                                                      \
+        cudaError_t _e = (expr);                                              \
+        if (_e != cudaSuccess)                                                \
+            return fail(TLB_ERR_CUDA, "%s: %s", #expr, cudaGetErrorString(_e)); \
+    } while (0)
+
+static int launch_check(const char *what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess)
+        return fail(TLB_ERR_CUDA, "%s launch: %s", what, cudaGetErrorString(e));
+    return TLB_OK;
+}
+
+static bool g_stencil_set[64];
+
+// --------------------------------------------------------- device helpers --
+struct Fld {
+    double *base;
+    long long sl, sx, sy;
+    int Lx, Ly, Hx, Hy;
+};
+
+static Fld mkfld(const TlbField *f) {
+    Fld d;
+    d.base = f->base;
+    d.sl = f->sl; d.sx = f->sx; d.sy = f->sy;
+    d.Lx = f->Lx; d.Ly = f->Ly; d.Hx = f->Hx; d.Hy = f->Hy;
+    return d;
+}
+
+static Phys mkphys(const TlbParams *p) {
+    // exactly the reference's host-side expressions (kernels.py:130-133, 145)
+    Phys P;
+    P.K1 = p->tau * p->gx;
+    P.K2 = p->tau * p->gy;
+    double g2 = p->gx * p->gx + p->gy * p->gy;
+    P.K3 = p->tau * p->tau * g2 / 2.0;
+    P.omega = p->dt / p->tau;
+    P.Tbot = p->Twall_bot;
+    P.Ttop = p->Twall_top;
+    P.order = p->order;
+    return P;
+}
+
+struct SiteLaunch {
+    Fld src, dst;
+    int x0, y0, ny;
+    long long nsites;
+    int bot_lo, bot_hi, top_lo, top_hi;  // bc rows (padded y), empty if lo>=hi
+    int flags;
+    Phys P;
+    TlbStatus *status;
+    int step;
+};
+
+__device__ __forceinline__ void report(TlbStatus *st, unsigned bits, int x, int y, int step) {
+    if (!bits || !st) return;
+    unsigned old = atomicOr(&st->flags, bits);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        if ((bits >> k & 1u) && !(old >> k & 1u)) {
+            st->site_x[k] = x;
+            st->site_y[k] = y;
+            st->step = step;
+        }
+    }
+}
+
+__device__ __forceinline__ void count_neg(TlbStatus *st, const double (&f)[Q], bool active) {
+    unsigned n = 0;
+    if (active) {
+#pragma unroll
+        for (int l = 0; l < Q; ++l) n += f[l] < 0.0;
+    }
+    n = __reduce_add_sync(0xffffffffu, n);
+    if ((threadIdx.x & 31) == 0 && n) atomicAdd(&st->negatives, (unsigned long long)n);
+}
+
+enum Kind { K_PROPAGATE = 0, K_BC = 1, K_COLLIDE = 2, K_FUSED = 3 };
+
+// Source coordinate of population l's pull for site (x, y) with implicit
+// halos (TLB_F_WRAP_X / WRAP_Y / CLAMP_Y), else the halo memory itself.
+__device__ __forceinline__ int src_x(int x, int cx, const Fld &s, int flags) {
+    int xs = x - cx;
+    if (flags & TLB_F_WRAP_X) {
+        if (xs < s.Hx) xs += s.Lx;
+        else if (xs >= s.Hx + s.Lx) xs -= s.Lx;
+    }
+    return xs;
+}
+__device__ __forceinline__ int src_y(int y, int cy, const Fld &s, int flags) {
+    int ys = y - cy;
+    if (flags & TLB_F_WRAP_Y) {
+        if (ys < s.Hy) ys += s.Ly;
+        else if (ys >= s.Hy + s.Ly) ys -= s.Ly;
+    } else if (flags & TLB_F_CLAMP_Y) {
+        ys = ys < s.Hy ? s.Hy : (ys >= s.Hy + s.Ly ? s.Hy + s.Ly - 1 : ys);
+    }
+    return ys;
+}
+
+template <int l>
+__device__ __forceinline__ void load_one(double (&f)[Q], const Fld &s, int x, int y,
+                                         bool gather, bool implicit, int flags) {
+    int xs = x, ys = y;
+    if (gather) {
+        if (implicit) {
+            xs = src_x(x, CX(l), s, flags);
+            ys = src_y(y, CY(l), s, flags);
+        } else {
+            xs = x - CX(l);
+            ys = y - CY(l);
+        }
+    }
+    const double *p = s.base + (long long)l * s.sl + (long long)xs * s.sx + (long long)ys * s.sy;
+    f[l] = __ldg(p);
+}
+
+template <int... Ls>
+struct LoadSeq {
+    __device__ __forceinline__ static void run(double (&f)[Q], const Fld &s, int x, int y,
+                                               bool gather, bool implicit, int flags) {
+        (load_one<Ls>(f, s, x, y, gather, implicit, flags), ...);
+    }
+};
+
+__device__ __forceinline__ void load_all(double (&f)[Q], const Fld &s, int x, int y,
+                                         bool gather, bool implicit, int flags) {
+    LoadSeq<0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16, 17, 18, 19, 20, 21,
+            22, 23, 24, 25, 26, 27, 28, 29, 30, 31, 32, 33, 34, 35,
+            36>::run(f, s, x, y, gather, implicit, flags);
+}
+
+__device__ __forceinline__ void store_all(const double (&f)[Q], const Fld &d, int x, int y) {
+    double *p = d.base + (long long)x * d.sx + (long long)y * d.sy;
+#pragma unroll
+    for (int l = 0; l < Q; ++l) p[(long long)l * d.sl] = f[l];
+}
+
+// In-place collide reads the same addresses it writes: plain loads, not the
+// non-coherent path.
+__device__ __forceinline__ void load_inplace(double (&f)[Q], const Fld &s, int x, int y) {
+    const double *p = s.base + (long long)x * s.sx + (long long)y * s.sy;
+#pragma unroll
+    for (int l = 0; l < Q; ++l) f[l] = p[(long long)l * s.sl];
+}
+
+// One thread = one site.  Sites are enumerated y-fastest over the region so
+// consecutive lanes touch consecutive addresses of every population plane.
+template <int KIND, bool EXACT, int ORDER, bool INPLACE>
+__global__ void __launch_bounds__(128) k_site(SiteLaunch L) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool active = i < L.nsites;
+    const long long ii = active ? i : L.nsites - 1;
+    const int x = L.x0 + (int)(ii / L.ny);
+    const int y = L.y0 + (int)(ii % L.ny);
+    double f[Q];
+    const bool gather = KIND == K_PROPAGATE || KIND == K_FUSED;
+    const bool implicit = (L.flags & (TLB_F_WRAP_X | TLB_F_WRAP_Y | TLB_F_CLAMP_Y)) != 0;
+    if (INPLACE)
+        load_inplace(f, L.src, x, y);
+    else
+        load_all(f, L.src, x, y, gather, implicit, L.flags);
+    unsigned bits = 0;
+    if (KIND == K_BC || KIND == K_FUSED) {
+        const bool bot = y >= L.bot_lo && y < L.bot_hi;
+        const bool top = y >= L.top_lo && y < L.top_hi;
+        if (bot || top) {
+            const double Tw = bot ? L.P.Tbot : L.P.Ttop;
+            bits |= EXACT ? bc_exact<ORDER>(f, Tw) : bc_fast<ORDER>(f, Tw);
+        }
+    }
+    if (KIND == K_COLLIDE || KIND == K_FUSED)
+        bits |= EXACT ? collide_exact<ORDER>(f, L.P) : collide_fast<ORDER>(f, L.P);
+    if (active) {
+        report(L.status, bits, x, y, L.step);
+        store_all(f, L.dst, x, y);
+    }
+    if (L.flags & TLB_F_COUNT_NEG) count_neg(L.status, f, active);
+}
+
+// --------------------------------------------------------------- launcher --
+template <int KIND, bool INPLACE>
+static int launch_site(SiteLaunch &L, bool exact, int order, cudaStream_t s, const char *what) {
+    if (L.nsites <= 0) return TLB_OK;
+    const int bs = 128;
+    const long long nb = (L.nsites + bs - 1) / bs;
+    if (nb > 0x7fffffffLL) return fail(TLB_ERR_CONTRACT, "%s: region too large", what);
+    dim3 grid((unsigned)nb), block(bs);
+#define TLB_L(E, O) k_site<KIND, E, O, INPLACE><<<grid, block, 0, s>>>(L)
+    if (exact) {
+        if (order == 4) TLB_L(true, 4);
+        else if (order == 3) TLB_L(true, 3);
+        else TLB_L(true, 2);
+    } else {
+        if (order == 4) TLB_L(false, 4);
+        else if (order == 3) TLB_L(false, 3);
+        else TLB_L(false, 2);
+    }
+#undef TLB_L
+    return launch_check(what);
+}
+
+static int check_params(const TlbParams *p) {
+    if (!p) return fail(TLB_ERR_CONTRACT, "null params");
+    if (p->order < 2 || p->order > 4)
+        return fail(TLB_ERR_DOMAIN, "unsupported expansion order %d", p->order);
+    if (!(p->tau > p->dt / 2))
+        return fail(TLB_ERR_DOMAIN, "tau=%g violates tau > dt/2", p->tau);
+    return TLB_OK;
+}
+
+static int check_stencil() {
+    int dev = 0;
+    TLB_CUDA_CHECK(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= 64 || !g_stencil_set[dev])
+        return fail(TLB_ERR_STENCIL, "stencil not set on device %d (call tlb_set_stencil)", dev);
+    return TLB_OK;
+}
+
+static int check_region(const TlbField *f, TlbRegion r, const char *what) {
+    if (r.x0 < f->Hx || r.x1 > f->Hx + f->Lx || r.y0 < f->Hy || r.y1 > f->Hy + f->Ly)
+        return fail(TLB_ERR_CONTRACT, "%s: region [%d,%d)x[%d,%d) extends into the halo", what,
+                    r.x0, r.x1, r.y0, r.y1);
+    return TLB_OK;
+}
+
+static void fill_region(SiteLaunch &L, TlbRegion r) {
+    L.x0 = r.x0;
+    L.y0 = r.y0;
+    L.ny = r.y1 > r.y0 ? r.y1 - r.y0 : 0;
+    const long long nx = r.x1 > r.x0 ? r.x1 - r.x0 : 0;
+    L.nsites = nx * L.ny;
+    if (L.ny == 0) L.ny = 1;
+}
+
+static void wall_rows(SiteLaunch &L, const TlbField *f, int flags) {
+    L.bot_lo = L.bot_hi = L.top_lo = L.top_hi = 0;
+    if (flags & TLB_F_WALL_BOT) {
+        L.bot_lo = f->Hy;
+        L.bot_hi = f->Hy + TLB_WALL_ROWS;
+    }
+    if (flags & TLB_F_WALL_TOP) {
+        L.top_lo = f->Hy + f->Ly - TLB_WALL_ROWS;
+        L.top_hi = f->Hy + f->Ly;
+    }
+}
+
+// --------------------------------------------------------- small kernels --
+__global__ void k_extend_walls(Fld f, int NX, int upper, int lower) {
+    // grid: (ceil(NX*Q/128)); each thread one (l, x) column, copies 2*Hy cells
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (long long)NX * Q) return;
+    const int l = (int)(i / NX), x = (int)(i % NX);
+    double *col = f.base + (long long)l * f.sl + (long long)x * f.sx;
+    const double top = col[(long long)(f.Hy + f.Ly - 1) * f.sy];
+    const double bot = col[(long long)f.Hy * f.sy];
+    for (int k = 0; k < f.Hy; ++k) {
+        if (upper) col[(long long)(f.Hy + f.Ly + k) * f.sy] = top;
+        if (lower) col[(long long)k * f.sy] = bot;
+    }
+}
+
+// Face-plan line table: for sign s (0 = +x, 1 = -x), line k -> (l, d).
+struct FaceLines {
+    int n;
+    int l[64], d[64];
+};
+
+static FaceLines face_lines(int sign, int axis) {
+    FaceLines t;
+    t.n = 0;
+    for (int d = 1; d <= 3; ++d)
+        for (int l = 0; l < Q; ++l) {
+            int c = axis == 0 ? CX(l) : CY(l);
+            if (sign * c >= d) {
+                t.l[t.n] = l;
+                t.d[t.n] = d;
+                ++t.n;
+            }
+        }
+    return t;
+}
+
+__device__ __forceinline__ int ysrc_mode(int y, const Fld &f, int ymode) {
+    if (ymode == 1) return y < f.Hy ? f.Hy : (y >= f.Hy + f.Ly ? f.Hy + f.Ly - 1 : y);
+    if (ymode == 2) return y < f.Hy ? y + f.Ly : (y >= f.Hy + f.Ly ? y - f.Ly : y);
+    return y;
+}
+
+// pack_x (runtime.py:199-208): buf[k*NY + y] = f[l_k, col(d_k), y]
+__global__ void k_pack_x(Fld f, FaceLines t, int sign, int ymode, double *buf) {
+    const int NY = f.Ly + 2 * f.Hy;
+    const int k = blockIdx.y;
+    const int y = blockIdx.x * blockDim.x + threadIdx.x;
+    if (y >= NY || k >= t.n) return;
+    const int d = t.d[k];
+    const int col = sign == 1 ? f.Hx + f.Lx - d : f.Hx + d - 1;
+    const int ys = ysrc_mode(y, f, ymode);
+    buf[(long long)k * NY + y] =
+        f.base[(long long)t.l[k] * f.sl + (long long)col * f.sx + (long long)ys * f.sy];
+}
+
+// unpack_x (runtime.py:210-224): sign +1 came from the left -> low-x halo
+__global__ void k_unpack_x(Fld f, FaceLines t, int sign, const double *buf) {
+    const int NY = f.Ly + 2 * f.Hy;
+    const int k = blockIdx.y;
+    const int y = blockIdx.x * blockDim.x + threadIdx.x;
+    if (y >= NY || k >= t.n) return;
+    const int d = t.d[k];
+    const int col = sign == 1 ? f.Hx - d : f.Hx + f.Lx - 1 + d;
+    f.base[(long long)t.l[k] * f.sl + (long long)col * f.sx + (long long)y * f.sy] =
+        buf[(long long)k * NY + y];
+}
+
+// pbc_c with self (both directions, one launch): halo col <- wrapped column
+__global__ void k_pbc_self_x(Fld f, FaceLines tp, FaceLines tm) {
+    const int NY = f.Ly + 2 * f.Hy;
+    const int k = blockIdx.y;
+    const int y = blockIdx.x * blockDim.x + threadIdx.x;
+    if (y >= NY) return;
+    const bool plus = k < tp.n;
+    const int kk = plus ? k : k - tp.n;
+    if (!plus && kk >= tm.n) return;
+    const int l = plus ? tp.l[kk] : tm.l[kk];
+    const int d = plus ? tp.d[kk] : tm.d[kk];
+    const int scol = plus ? f.Hx + f.Lx - d : f.Hx + d - 1;
+    const int dcol = plus ? f.Hx - d : f.Hx + f.Lx - 1 + d;
+    double *pl = f.base + (long long)l * f.sl + (long long)y * f.sy;
+    pl[(long long)dcol * f.sx] = pl[(long long)scol * f.sx];
+}
+
+// pbc_nc with self (periodic Y, physical columns only, runtime.py:226-267)
+__global__ void k_pbc_self_y(Fld f, FaceLines tp, FaceLines tm) {
+    const int k = blockIdx.y;
+    const int xi = blockIdx.x * blockDim.x + threadIdx.x;
+    if (xi >= f.Lx) return;
+    const int x = f.Hx + xi;
+    const bool plus = k < tp.n;
+    const int kk = plus ? k : k - tp.n;
+    if (!plus && kk >= tm.n) return;
+    const int l = plus ? tp.l[kk] : tm.l[kk];
+    const int e = plus ? tp.d[kk] : tm.d[kk];
+    const int srow = plus ? f.Hy + f.Ly - e : f.Hy + e - 1;
+    const int drow = plus ? f.Hy - e : f.Hy + f.Ly - 1 + e;
+    double *pc = f.base + (long long)l * f.sl + (long long)x * f.sx;
+    pc[(long long)drow * f.sy] = pc[(long long)srow * f.sy];
+}
+
+// halo from peer fields (face-plan lines, full NY)
+__global__ void k_halo_from_peers(Fld f, Fld left, Fld right, FaceLines tp, FaceLines tm) {
+    const int NY = f.Ly + 2 * f.Hy;
+    const int k = blockIdx.y;
+    const int y = blockIdx.x * blockDim.x + threadIdx.x;
+    if (y >= NY) return;
+    const bool plus = k < tp.n;  // data travelling +x: from the left peer
+    const int kk = plus ? k : k - tp.n;
+    if (!plus && kk >= tm.n) return;
+    const int l = plus ? tp.l[kk] : tm.l[kk];
+    const int d = plus ? tp.d[kk] : tm.d[kk];
+    const Fld &src = plus ? left : right;
+    const int scol = plus ? src.Hx + src.Lx - d : src.Hx + d - 1;
+    const int dcol = plus ? f.Hx - d : f.Hx + f.Lx - 1 + d;
+    f.base[(long long)l * f.sl + (long long)dcol * f.sx + (long long)y * f.sy] =
+        src.base[(long long)l * src.sl + (long long)scol * src.sx + (long long)y * src.sy];
+}
+
+template <bool EXACT>
+__global__ void k_moments(Fld f, int x0, int y0, int ny, long long n, double *rho, double *ux,
+                          double *uy, double *T, long long ld, int check, TlbStatus *st) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int xi = (int)(i / ny), yi = (int)(i % ny);
+    double fl[Q];
+    const double *p = f.base + (long long)(x0 + xi) * f.sx + (long long)(y0 + yi) * f.sy;
+#pragma unroll
+    for (int l = 0; l < Q; ++l) fl[l] = p[(long long)l * f.sl];
+    double r, u, v, t;
+    bool ok = moments_exact(fl, r, u, v, t);
+    const long long o = (long long)xi * ld + yi;
+    rho[o] = r; ux[o] = u; uy[o] = v; T[o] = t;
+    if (check && !ok) report(st, 1u, x0 + xi, y0 + yi, -1);
+}
+
+template <bool EXACT, int ORDER>
+__global__ void k_equilibrium(const double *rho, const double *ux, const double *uy,
+                              const double *T, long long n, double *out, long long ld,
+                              int check, TlbStatus *st) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double r = rho[i], u = ux[i], v = uy[i], t = T[i];
+    if (check && (!(r > 0.0) || !(t > 0.0))) report(st, 4u, (int)i, 0, -1);
+    double f[Q];
+#pragma unroll
+    for (int l = 0; l < Q; ++l) f[l] = 0.0;
+    if (EXACT) {
+        const EqSite e = eq_site_exact(r, u, v, t);
+        eq_all_exact<ORDER, 0>(f, e, 0.0);
+    } else {
+        FastSite e;
+        e.vx = u * C.rcs;
+        e.vy = v * C.rcs;
+        e.theta = fma(t, C.rcs2, -1.0);
+        e.s = fma(e.vx, e.vx, e.vy * e.vy);
+        e.W = r;
+        fast_all<ORDER, 0>(f, e, 0.0);
+    }
+#pragma unroll
+    for (int l = 0; l < Q; ++l) out[(long long)l * ld + i] = f[l];
+}
+
+__global__ void k_apply_shift(const double *ux, const double *uy, const double *T, long long n,
+                              Phys P, double *ub, double *vb, double *Tb, TlbStatus *st) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    ub[i] = tlb::dadd(ux[i], P.K1);
+    vb[i] = tlb::dadd(uy[i], P.K2);
+    const double t = tlb::dsub(T[i], P.K3);
+    Tb[i] = t;
+    if (!(t > 0.0)) report(st, 2u, (int)i, 0, -1);
+}
+
+__global__ void k_count_negative(Fld f, int x0, int y0, int ny, long long n, TlbStatus *st) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    double fl[Q];
+    const bool active = i < n;
+    if (active) {
+        const int x = x0 + (int)(i / ny), y = y0 + (int)(i % ny);
+        const double *p = f.base + (long long)x * f.sx + (long long)y * f.sy;
+#pragma unroll
+        for (int l = 0; l < Q; ++l) fl[l] = p[(long long)l * f.sl];
+    }
+    count_neg(st, fl, active);
+}
+
+// ================================================================ C ABI ==
+extern "C" {
+
+int tlb_version(void) { return 1; }
+
+const char *tlb_last_error(void) { return g_msg.c_str(); }
+
+int tlb_set_device(int device) {
+    TLB_CUDA_CHECK(cudaSetDevice(device));
+    return TLB_OK;
+}
+
+int tlb_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+int tlb_set_stencil(int device, const int64_t *c, const double *w, double cs2) {
+    if (!c || !w) return fail(TLB_ERR_CONTRACT, "null stencil");
+    for (int l = 0; l < Q; ++l)
+        if (c[2 * l] != CX(l) || c[2 * l + 1] != CY(l))
+            return fail(TLB_ERR_STENCIL,
+                        "velocity %d is (%lld,%lld); this build is specialised for the "
+                        "reference D2Q37 ordering (velocity_set.py:55-59)",
+                        l, (long long)c[2 * l], (long long)c[2 * l + 1]);
+    StencilConst h;
+    memset(&h, 0, sizeof h);
+    h.cs2 = cs2;
+    h.cs = std::sqrt(cs2);  // np.sqrt(vs.cs2)             kernels.py:87
+    for (int k = 0; k < 4; ++k) h.E[k] = (double)k / h.cs;  // c/cs  kernels.py:95
+    for (int sh = 0; sh < NSHELL; ++sh) {
+        const int l0 = SH_START(sh);
+        const double ex = (double)CX(l0) / h.cs, ey = (double)CY(l0) / h.cs;
+        h.qsh[sh] = ex * ex + ey * ey;                      // kernels.py:97
+        h.wsh[sh] = w[l0];
+        for (int l = l0; l < l0 + SH_N(sh); ++l) {
+            const double exl = (double)CX(l) / h.cs, eyl = (double)CY(l) / h.cs;
+            if (exl * exl + eyl * eyl != h.qsh[sh] || w[l] != w[l0])
+                return fail(TLB_ERR_STENCIL, "weights/speeds not constant on shell %d", sh);
+        }
+    }
+    h.rcs = 1.0 / h.cs;
+    h.rcs2 = 1.0 / cs2;
+    h.r6 = 1.0 / 6.0;
+    h.r24 = 1.0 / 24.0;
+    h.set = 1;
+    if (device < 0 || device >= 64) return fail(TLB_ERR_CONTRACT, "bad device %d", device);
+    TLB_CUDA_CHECK(cudaSetDevice(device));
+    TLB_CUDA_CHECK(cudaMemcpyToSymbol(C, &h, sizeof h));
+    TLB_CUDA_CHECK(cudaDeviceSynchronize());
+    g_stencil_set[device] = true;
+    return TLB_OK;
+}
+
+int tlb_propagate(const TlbField *prv, const TlbField *nxt, TlbRegion r, tlb_stream_t stream) {
+    int e;
+    if ((e = check_stencil())) return e;
+    if ((e = check_region(prv, r, "propagate"))) return e;
+    SiteLaunch L;
+    memset(&L, 0, sizeof L);
+    L.src = mkfld(prv);
+    L.dst = mkfld(nxt);
+    fill_region(L, r);
+    return launch_site<K_PROPAGATE, false>(L, true, 4, (cudaStream_t)stream, "propagate");
+}
+
+int tlb_bc(const TlbField *f, const TlbParams *p, int top, int bottom, int32_t x0, int32_t x1,
+           TlbStatus *status, tlb_stream_t stream) {
+    int e;
+    if ((e = check_stencil())) return e;
+    if (!p || p->order < 2 || p->order > 4)
+        return fail(TLB_ERR_DOMAIN, "unsupported expansion order");
+    if ((top && !(p->Twall_top > 0.0)) || (bottom && !(p->Twall_bot > 0.0)))
+        return fail(TLB_ERR_DOMAIN, "equilibrium requires rho > 0 and T > 0");
+    if (x0 < f->Hx || x1 > f->Hx + f->Lx)
+        return fail(TLB_ERR_CONTRACT, "bc: x_range extends into the halo");
+    const int flags = (top ? TLB_F_WALL_TOP : 0) | (bottom ? TLB_F_WALL_BOT : 0);
+    SiteLaunch L;
+    memset(&L, 0, sizeof L);
+    L.src = L.dst = mkfld(f);
+    L.P = mkphys(p);
+    L.status = status;
+    L.step = -1;
+    wall_rows(L, f, flags);
+    // bottom rows then top rows (kernels.py:190-203); a lattice with Ly < 6
+    // has overlapping wall rows -> run the walls as two ordered launches.
+    for (int side = 0; side < 2; ++side) {
+        if (side == 0 && !bottom) continue;
+        if (side == 1 && !top) continue;
+        SiteLaunch S = L;
+        if (side == 0) { S.top_lo = S.top_hi = 0; }
+        else { S.bot_lo = S.bot_hi = 0; }
+        TlbRegion r = {x0, x1, side == 0 ? S.bot_lo : S.top_lo, side == 0 ? S.bot_hi : S.top_hi};
+        fill_region(S, r);
+        if ((e = launch_site<K_BC, true>(S, p->arith == TLB_ARITH_EXACT, p->order,
+                                         (cudaStream_t)stream, "bc")))
+            return e;
+    }
+    return TLB_OK;
+}
+
+int tlb_collide(const TlbField *in, const TlbField *out, TlbRegion r, const TlbParams *p,
+                int flags, TlbStatus *status, tlb_stream_t stream) {
+    int e;
+    if ((e = check_stencil())) return e;
+    if ((e = check_params(p))) return e;
+    if ((e = check_region(in, r, "collide"))) return e;
+    if ((e = check_region(out, r, "collide"))) return e;
+    SiteLaunch L;
+    memset(&L, 0, sizeof L);
+    L.src = mkfld(in);
+    L.dst = mkfld(out);
+    L.P = mkphys(p);
+    L.status = status;
+    L.flags = flags & TLB_F_COUNT_NEG;
+    L.step = -1;
+    fill_region(L, r);
+    const bool inplace = in->base == out->base;
+    if (inplace)
+        return launch_site<K_COLLIDE, true>(L, p->arith == TLB_ARITH_EXACT, p->order,
+                                            (cudaStream_t)stream, "collide");
+    return launch_site<K_COLLIDE, false>(L, p->arith == TLB_ARITH_EXACT, p->order,
+                                         (cudaStream_t)stream, "collide");
+}
+
+int tlb_fused(const TlbField *prv, const TlbField *nxt, TlbRegion r, const TlbParams *p,
+              int flags, TlbStatus *status, tlb_stream_t stream) {
+    int e;
+    if ((e = check_stencil())) return e;
+    if ((e = check_params(p))) return e;
+    if ((e = check_region(prv, r, "fused"))) return e;
+    if ((flags & TLB_F_WALL_TOP) && !(p->Twall_top > 0.0))
+        return fail(TLB_ERR_DOMAIN, "equilibrium requires rho > 0 and T > 0");
+    if ((flags & TLB_F_WALL_BOT) && !(p->Twall_bot > 0.0))
+        return fail(TLB_ERR_DOMAIN, "equilibrium requires rho > 0 and T > 0");
+    if (prv->base == nxt->base) return fail(TLB_ERR_CONTRACT, "fused: prv and nxt alias");
+    SiteLaunch L;
+    memset(&L, 0, sizeof L);
+    L.src = mkfld(prv);
+    L.dst = mkfld(nxt);
+    L.P = mkphys(p);
+    L.status = status;
+    L.flags = flags;
+    L.step = -1;
+    wall_rows(L, prv, flags);
+    fill_region(L, r);
+    return launch_site<K_FUSED, false>(L, p->arith == TLB_ARITH_EXACT, p->order,
+                                       (cudaStream_t)stream, "fused");
+}
+
+int tlb_step_self(const TlbField *prv, const TlbField *nxt, const TlbParams *p, int walls,
+                  int periodic_y, int count_neg, TlbStatus *status, tlb_stream_t stream) {
+    int flags = TLB_F_WRAP_X;
+    if (walls) flags |= TLB_F_WALL_BOT | TLB_F_WALL_TOP | TLB_F_CLAMP_Y;
+    else if (periodic_y) flags |= TLB_F_WRAP_Y;
+    if (count_neg) flags |= TLB_F_COUNT_NEG;
+    TlbRegion r = {prv->Hx, prv->Hx + prv->Lx, prv->Hy, prv->Hy + prv->Ly};
+    return tlb_fused(prv, nxt, r, p, flags, status, stream);
+}
+
+int tlb_moments(const TlbField *f, TlbRegion r, double *rho, double *ux, double *uy, double *T,
+                int64_t ld, int check, TlbStatus *status, tlb_stream_t stream) {
+    int e;
+    if ((e = check_stencil())) return e;
+    const int ny = r.y1 - r.y0;
+    const long long n = (long long)(r.x1 - r.x0) * ny;
+    if (n <= 0) return TLB_OK;
+    Fld d = mkfld(f);
+    k_moments<true><<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
+        d, r.x0, r.y0, ny, n, rho, ux, uy, T, ld, check, status);
+    return launch_check("moments");
+}
+
+int tlb_equilibrium(const double *rho, const double *ux, const double *uy, const double *T,
+                    int64_t n, int order, int arith, double *out, int64_t ld, int check,
+                    TlbStatus *status, tlb_stream_t stream) {
+    int e;
+    if ((e = check_stencil())) return e;
+    if (order < 2 || order > 4) return fail(TLB_ERR_DOMAIN, "unsupported expansion order %d", order);
+    if (n <= 0) return TLB_OK;
+    const unsigned nb = (unsigned)((n + 127) / 128);
+    cudaStream_t s = (cudaStream_t)stream;
+#define TLB_E(E, O) k_equilibrium<E, O><<<nb, 128, 0, s>>>(rho, ux, uy, T, n, out, ld, check, status)
+    if (arith == TLB_ARITH_EXACT) {
+        if (order == 4) TLB_E(true, 4); else if (order == 3) TLB_E(true, 3); else TLB_E(true, 2);
+    } else {
+        if (order == 4) TLB_E(false, 4); else if (order == 3) TLB_E(false, 3); else TLB_E(false, 2);
+    }
+#undef TLB_E
+    return launch_check("equilibrium");
+}
+
+int tlb_apply_shift(const double *ux, const double *uy, const double *T, int64_t n,
+                    const TlbParams *p, double *ub, double *vb, double *Tb, TlbStatus *status,
+                    tlb_stream_t stream) {
+    if (n <= 0) return TLB_OK;
+    k_apply_shift<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
+        ux, uy, T, n, mkphys(p), ub, vb, Tb, status);
+    return launch_check("apply_shift");
+}
+
+int tlb_count_negative(const TlbField *f, TlbRegion r, TlbStatus *status, tlb_stream_t stream) {
+    const int ny = r.y1 - r.y0;
+    const long long n = (long long)(r.x1 - r.x0) * ny;
+    if (n <= 0) return TLB_OK;
+    k_count_negative<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
+        mkfld(f), r.x0, r.y0, ny, n, status);
+    return launch_check("count_negative");
+}
+
+int tlb_extend_walls(const TlbField *f, int upper, int lower, tlb_stream_t stream) {
+    const int NX = f->Lx + 2 * f->Hx;
+    const long long n = (long long)NX * Q;
+    k_extend_walls<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(mkfld(f), NX,
+                                                                                  upper, lower);
+    return launch_check("extend_walls");
+}
+
+int64_t tlb_face_payload_len(const TlbField *f) {
+    return (int64_t)face_lines(1, 0).n * (f->Ly + 2 * f->Hy);
+}
+
+int tlb_pack_x(const TlbField *f, int sign, int ymode, double *buf, tlb_stream_t stream) {
+    if (sign != 1 && sign != -1) return fail(TLB_ERR_CONTRACT, "sign must be +-1");
+    FaceLines t = face_lines(sign, 0);
+    const int NY = f->Ly + 2 * f->Hy;
+    dim3 grid((NY + 127) / 128, t.n);
+    k_pack_x<<<grid, 128, 0, (cudaStream_t)stream>>>(mkfld(f), t, sign, ymode, buf);
+    return launch_check("pack_x");
+}
+
+int tlb_unpack_x(const TlbField *f, int sign, const double *buf, tlb_stream_t stream) {
+    if (sign != 1 && sign != -1) return fail(TLB_ERR_CONTRACT, "sign must be +-1");
+    FaceLines t = face_lines(sign, 0);
+    const int NY = f->Ly + 2 * f->Hy;
+    dim3 grid((NY + 127) / 128, t.n);
+    k_unpack_x<<<grid, 128, 0, (cudaStream_t)stream>>>(mkfld(f), t, sign, buf);
+    return launch_check("unpack_x");
+}
+
+int tlb_pbc_self_x(const TlbField *f, tlb_stream_t stream) {
+    FaceLines tp = face_lines(1, 0), tm = face_lines(-1, 0);
+    const int NY = f->Ly + 2 * f->Hy;
+    dim3 grid((NY + 127) / 128, tp.n + tm.n);
+    k_pbc_self_x<<<grid, 128, 0, (cudaStream_t)stream>>>(mkfld(f), tp, tm);
+    return launch_check("pbc_self_x");
+}
+
+int tlb_pbc_self_y(const TlbField *f, tlb_stream_t stream) {
+    FaceLines tp = face_lines(1, 1), tm = face_lines(-1, 1);
+    dim3 grid((f->Lx + 127) / 128, tp.n + tm.n);
+    k_pbc_self_y<<<grid, 128, 0, (cudaStream_t)stream>>>(mkfld(f), tp, tm);
+    return launch_check("pbc_self_y");
+}
+
+int tlb_halo_from_peers(const TlbField *f, const TlbField *left, const TlbField *right,
+                        tlb_stream_t stream) {
+    FaceLines tp = face_lines(1, 0), tm = face_lines(-1, 0);
+    const int NY = f->Ly + 2 * f->Hy;
+    dim3 grid((NY + 127) / 128, tp.n + tm.n);
+    k_halo_from_peers<<<grid, 128, 0, (cudaStream_t)stream>>>(mkfld(f), mkfld(left), mkfld(right),
+                                                              tp, tm);
+    return launch_check("halo_from_peers");
+}
+
+}  // extern "C"

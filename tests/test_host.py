@@ -1,0 +1,164 @@
+"""Host-side logic and the C ABI surface -- CPU only (no GPU needed)."""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, golden
+
+import paper_1703_00185_b200 as tl
+from paper_1703_00185_b200 import _lib
+
+
+# ---------------------------------------------------------- velocity set --
+
+def test_velocity_set_matches_reference_bits(stencil):
+    vs = tl.build_velocity_set("D2Q37")
+    assert np.array_equal(vs.c, stencil["c"])
+    assert np.array_equal(vs.w, stencil["w"])
+    assert vs.cs2 == float(stencil["cs2"])
+    assert vs.max_hop == 3 and vs.eq_order == 4
+
+
+def test_velocity_set_invariants():
+    vs = tl.build_velocity_set("D2Q37")
+    c = vs.c.astype(float)
+    assert abs(vs.w.sum() - 1.0) < 1e-12
+    assert np.all(vs.w > 0)
+    # closed under negation; partner of l within its shell is n-1-i
+    for l in range(37):
+        assert vs.find(-vs.c[l, 0], -vs.c[l, 1]) is not None
+    assert abs(np.sum(vs.w * c[:, 0] * c[:, 0]) - vs.cs2) < 1e-12
+
+
+def test_unknown_model():
+    with pytest.raises(tl.ConfigurationError):
+        tl.build_velocity_set("D3Q19")
+
+
+# -------------------------------------------------------------- geometry --
+
+def test_padding_and_extents():
+    g = tl.LatticeGeometry(1024, 8192, 3, 3, 37)
+    assert (g.NX, g.NY) == (1030, 8198)   # reference test_geometry.py:19-22
+    assert g.phys_x == slice(3, 1027)
+
+
+def test_site_index_layouts():
+    g = tl.LatticeGeometry(4, 4, 3, 3, 9, tl.SOA)
+    assert tl.site_index(g, 0, 0, 0) == 0
+    assert tl.site_index(g, 1, 0, 0) == g.NX * g.NY
+    assert tl.site_index(g, 0, 1, 0) == g.NY
+    ga = tl.LatticeGeometry(4, 4, 3, 3, 9, tl.AOS)
+    x, y = divmod(5, ga.NY)
+    assert tl.site_index(ga, 2, x, y) == 5 * ga.Q + 2
+    with pytest.raises(tl.ContractViolation):
+        tl.site_index(g, 9, 0, 0)
+
+
+def test_degenerate_geometry():
+    with pytest.raises(tl.AllocationError):
+        tl.LatticeGeometry(0, 4, 3, 3, 9)
+    with pytest.raises(tl.AllocationError):
+        tl.LatticeGeometry(4, 4, 3, 3, 9, "soa_bogus")
+
+
+# --------------------------------------------------------------- runtime --
+
+def test_decompose_1d_ring():
+    tiles = tl.decompose(64, 32, 4, "1d")
+    assert [t.x0 for t in tiles] == [0, 16, 32, 48]
+    assert tiles[0].neighbors["left"] == 3 and tiles[3].neighbors["right"] == 0
+    assert all(t.uppermost and t.lowermost for t in tiles)
+
+
+def test_decompose_rejects_indivisible():
+    with pytest.raises(tl.ConfigurationError, match="divides only by"):
+        tl.decompose(100, 100, 3, "1d")
+
+
+def test_face_plans_d2q37():
+    vs = tl.build_velocity_set("D2Q37")
+    plans = tl.face_plans(vs)
+    for key in plans:
+        assert [len(x) for x in plans[key]] == [15, 8, 3]
+    assert list(plans[(0, 1)][2]) == [28, 35, 36]
+    assert tl.boundary_bytes_per_site(vs) == 208
+
+
+def test_fabric_protocol():
+    fab = tl.Fabric(2, timeout=0.2)
+    fab.send(0, 1, "x+", 3, "payload")
+    with pytest.raises(tl.ProtocolError, match="expected step 4"):
+        fab.recv(1, 0, "x+", 4)
+    with pytest.raises(tl.DeadlockError, match="rank 1 stalled") as e:
+        fab.recv(1, 0, "x+", 0)
+    assert e.value.rank == 1
+    fab.send(0, 1, "x-", 7, "ok")
+    assert fab.recv(1, 0, "x-", 7) == "ok"
+
+
+def test_simconfig_validation():
+    with pytest.raises(tl.ConfigurationError):
+        tl.SimConfig(Lx=8, Ly=8, schedule="bogus")
+    with pytest.raises(tl.ConfigurationError):
+        tl.SimConfig(Lx=8, Ly=8, walls=True, periodic_y=True)
+
+
+def test_physics_params_validation():
+    with pytest.raises(tl.DomainError):
+        tl.PhysicsParams(tau=0.4)
+    with pytest.raises(tl.DomainError):
+        tl.PhysicsParams(tau=1.0, arith="bogus")
+
+
+# ------------------------------------------------------------- the C ABI --
+
+def _header_functions():
+    src = open(os.path.join(ROOT, "include", "tlb.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(tlb_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_library_exports_every_header_symbol():
+    lib = _lib.load()          # loads without a GPU
+    names = _header_functions()
+    assert len(names) >= 20
+    for n in names:
+        assert hasattr(lib, n), n
+    bound = {s[0] for s in _lib.SIGNATURES}
+    assert set(names) == bound
+
+
+def test_struct_layouts_match_header():
+    assert ctypes.sizeof(_lib.TlbField) == 8 + 3 * 8 + 4 * 4
+    assert ctypes.sizeof(_lib.TlbParams) == 6 * 8 + 2 * 4
+    assert ctypes.sizeof(_lib.TlbStatus) == 48
+    assert _lib.TlbStatus.negatives.offset == 40
+
+
+def test_no_gpu_fails_loudly():
+    torch = pytest.importorskip("torch")
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(tl.DeviceError):
+        tl.run(tl.SimConfig(Lx=8, Ly=8, steps=1))
+    with pytest.raises(tl.DeviceError):
+        tl.collide(np.ones((37, 2)), tl.PhysicsParams(tau=0.8),
+                   tl.build_velocity_set("D2Q37"))
+    lib = _lib.load()
+    assert lib.tlb_device_count() == 0
+
+
+def test_product_does_not_import_oracle():
+    pkg = os.path.join(ROOT, "paper_1703_00185_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert "oracle" not in txt.replace("oracle/", "").lower() or \
+                    "import oracle" not in txt, f
+                assert "from oracle" not in txt and "import oracle" not in txt, f
