@@ -1,0 +1,412 @@
+#!/usr/bin/env python
+"""D2Q37 thermal-LBM time-step benchmark (BASELINE.json metric).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+A "step" is one full time step (X-halo exchange + propagate + bc + collide,
+fused) of the whole lattice.  At N=1 the workload is BASELINE.json configs[1]
+(D2Q37 Rayleigh-Taylor 1920x2048 on one B200); at N>1 it is configs[2]
+(weak scaling, 1920x2048 per GPU, 1-D X tiling, overlapped halo exchange
+over NCCL), one process per GPU under torchrun.  Prints ONE JSON line on
+rank 0.
+
+--impl reference times the reference algorithm on the host CPU (the C
+oracle restatement, all host threads) on a bounded sample of the workload.
+"""
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MLUPS and FP64 sustained GFLOPS per step at 1/2/4/8 B200 vs roofline and CPU ref"
+FLOP_SITE = 2764          # collide, algorithmic
+FLOP_WALL_SITE = 2449     # bc, per wall-row site
+BYTES_SITE = 592          # fused step: 37 x 8 B read + 37 x 8 B written
+TILE_LX, TILE_LY = 1920, 2048
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh)
+    except OSError:
+        return {}
+
+
+# ----------------------------------------------------------------- clocks --
+
+class ClockSampler:
+    """nvidia-smi sampled every 100 ms during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap,utilization.gpu")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+
+    def __init__(self, gpu_id):
+        self.gpu_id = gpu_id
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-i", str(self.gpu_id)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        for r in self.rows:
+            try:
+                util = float(r[7])
+            except ValueError:
+                util = 100.0
+            if util < 50:
+                continue
+            try:
+                sm.append(float(r[0]))
+                smax.append(float(r[1]))
+            except ValueError:
+                continue
+            for name, v in zip(self.NAMES, r[3:7]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(smax),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------ CPU oracle --
+
+def cpu_oracle_rate(seconds, steps=None, warmup=0, Lx=240, Ly=TILE_LY):
+    """C oracle (oracle/tlb_oracle.c, bitwise = the reference) with all host
+    threads on an RT Lx x Ly sample lattice.  Returns (MLUPS, threads,
+    steps, sample description)."""
+    from oracle import oracle as O
+    import paper_1703_00185_b200 as tl
+    O.build()
+    vs = tl.build_velocity_set("D2Q37")
+    O.set_stencil(vs.c, vs.w, vs.cs2)
+    nthreads = len(os.sched_getaffinity(0))
+    O.threads(nthreads)
+    p6 = O.params6(0.8, 0.0, -1e-5, 1.0, 0.9 * vs.cs2, 1.1 * vs.cs2)
+    f0 = O.equilibrium(*O.rayleigh_taylor_macro(Lx, Ly, vs.cs2))
+    t1 = time.perf_counter()
+    f0, _ = O.run(f0, max(warmup, 1), p6)     # warm-up (also sizes the sample)
+    per_step = (time.perf_counter() - t1) / max(warmup, 1)
+    done = steps if steps is not None else max(3, int(seconds / per_step))
+    t0 = time.perf_counter()
+    f, _ = O.run(f0, done, p6)                # one call: buffers allocated once
+    el = time.perf_counter() - t0
+    return (Lx * Ly * done / el / 1e6, nthreads, done,
+            f"RT {Lx}x{Ly} sample lattice (walls, periodic X), {done} steps, "
+            f"{nthreads} threads, {el:.1f} s")
+
+
+def reference_arm(args, rank, world):
+    if rank != 0:
+        return 0
+    mlups, nthreads, done, sample = cpu_oracle_rate(None, steps=args.steps, warmup=args.warmup)
+    Lx = TILE_LX * world
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(mlups, 4), "unit": "MLUPS",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (Rayleigh-Taylor init)",
+        "config": {"workload": f"D2Q37 RT {Lx}x{TILE_LY} (1-D X tiles of {TILE_LX}x{TILE_LY})",
+                   "sample": sample},
+        "gflops_fp64": round(mlups * FLOP_SITE / 1e3, 3),
+        "cpu_baseline": {"value": round(mlups, 4), "unit": "MLUPS", "cores": nthreads,
+                         "kind": "port", "sample": sample},
+        "e2e": {"value": round(mlups, 4), "unit": "MLUPS", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------- GPU arm --
+
+def gpu_arm(args, rank, world, local_rank):
+    import torch
+    import paper_1703_00185_b200 as tl
+    from paper_1703_00185_b200 import _lib
+    from paper_1703_00185_b200.kernels import field_desc
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    vs = tl.build_velocity_set("D2Q37")
+    Lx_tile, Ly = args.Lx, args.Ly
+    Lx = Lx_tile * world
+    p = tl.PhysicsParams(tau=0.8, gx=0.0, gy=-1e-5, Twall_top=0.9 * vs.cs2,
+                         Twall_bot=1.1 * vs.cs2, arith=args.arith)
+    tiles = tl.decompose(Lx, Ly, world, "1d")
+    tile = tiles[rank]
+    fabric = tl.DistFabric() if world > 1 else tl.Fabric(1)
+    w = tl.RankWorker(tile, vs, p, fabric, schedule=args.schedule, device=dev)
+    macro = tl.init.rayleigh_taylor_macro(Lx, Ly, vs)
+    sl = slice(tile.x0, tile.x0 + Lx_tile)
+    f0 = tl.equilibrium(*[torch.as_tensor(np.ascontiguousarray(a[sl]), device=dev)
+                          for a in macro], vs)
+    w.load_block(f0)
+    torch.cuda.synchronize()
+
+    def barrier():
+        if dist is not None:
+            dist.barrier(device_ids=[local_rank])
+
+    def run_steps(n, s0=0):
+        for s in range(s0, s0 + n):
+            w.step(s)
+
+    # warm-up
+    run_steps(args.warmup)
+    w.synchronize()
+    w.collect()
+    w._metrics.clear()
+
+    # clocks: sample while a ~1 s untimed pre-load runs, then the timed steps
+    sampler = ClockSampler(_gpu_index(local_rank))
+    sampler.start()
+    t_pre = time.perf_counter()
+    s = args.warmup
+    while time.perf_counter() - t_pre < args.preload:
+        run_steps(10, s)
+        s += 10
+        w.synchronize()
+    w.collect()
+    w._metrics.clear()
+
+    barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(w.stream)
+    run_steps(args.steps, s)
+    e1.record(w.stream)
+    torch.cuda.synchronize()
+    barrier()
+    clocks = sampler.stop()
+    ms = e0.elapsed_time(e1)
+    if dist is not None:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    metrics = w.metrics
+    bulk_ms = [m["t_bulk"] * 1e3 for m in metrics]
+    sites = Lx * Ly
+    mlups = sites * args.steps / (ms * 1e-3) / 1e6
+    flops_step = FLOP_SITE * sites + FLOP_WALL_SITE * 6 * Lx
+    gflops = flops_step * args.steps / (ms * 1e-3) / 1e9
+
+    # dominant kernel: the fused step over the (bulk) region of this rank
+    h = 3
+    kern_sites = (Lx_tile if world == 1 else Lx_tile - 2 * h) * Ly
+    kern_ms = float(np.mean(bulk_ms))
+    achieved = BYTES_SITE * kern_sites / (kern_ms * 1e-3) / 1e9
+    pk = peaks()
+    hbm_peak = pk.get("hbm_gbs")
+    peak_src = "MEASURED_PEAKS.json hbm_gbs (measured copy)"
+    if hbm_peak is None:
+        hbm_peak, peak_src = 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+    out = None
+    if rank == 0:
+        lib = _lib.load()
+        import ctypes
+        fp = ctypes.c_double(0.0)
+        _lib.check(lib.tlb_bench_dfma(200000, ctypes.byref(fp), _lib.stream_ptr()), "dfma")
+        fp64_peak = fp.value / 1e12
+        kern_tflops = (FLOP_SITE * kern_sites + FLOP_WALL_SITE * 6 * Lx_tile) / (kern_ms * 1e-3) / 1e12
+        split = split_kernels(w, tl, _lib, field_desc, torch) if args.split else None
+        out = {
+            "metric": METRIC, "value": round(mlups, 3), "unit": "MLUPS",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms / args.steps, 5), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (Rayleigh-Taylor initial state, reference init.py:45-64)",
+            "config": {"workload": f"D2Q37 RT {Lx}x{Ly}" + (
+                f" (1-D X tiles of {Lx_tile}x{Ly}, overlapped NCCL halo)" if world > 1 else
+                " on 1 B200 (BASELINE configs[1])"),
+                "Lx": Lx, "Ly": Ly, "tiling": "1d", "schedule": args.schedule,
+                "arith": args.arith, "tau": 0.8, "gy": -1e-5,
+                "l2": "no flush: 2 x %.2f GB state per GPU >> 126 MB L2" % (
+                    37 * (Lx_tile + 6) * (Ly + 6) * 8 / 1e9)},
+            "gflops_fp64": round(gflops, 2),
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak,
+                         "unit": "GB/s", "frac": round(achieved / hbm_peak, 4),
+                         "traffic": None, "kernel": "k_site<FUSED> (propagate+bc+collide)",
+                         "bytes_per_site": BYTES_SITE, "sites_per_launch": kern_sites,
+                         "avg_launch_ms": round(kern_ms, 5), "peak_source": peak_src,
+                         "fp64": {"achieved_tflops": round(kern_tflops, 3),
+                                  "peak_tflops_measured_dfma": round(fp64_peak, 3),
+                                  "frac": round(kern_tflops / fp64_peak, 4),
+                                  "flops_per_site": FLOP_SITE}},
+            "clocks": clocks,
+            "gpu_launches": args.steps * (1 if world == 1 else 7),
+        }
+        if split:
+            out["split"] = split
+    # e2e through the public API with host buffers
+    e2e = e2e_run(args, w, tl, torch, dist, local_rank, Lx_tile, Ly) if args.e2e else None
+    if rank == 0:
+        out["e2e"] = e2e
+        if world == 1 and args.cpu_seconds > 0:
+            mlups_cpu, nthreads, done, sample = cpu_oracle_rate(args.cpu_seconds)
+            out["cpu_baseline"] = {"value": round(mlups_cpu, 4), "unit": "MLUPS",
+                                   "cores": nthreads, "kind": "port", "sample": sample}
+        print(json.dumps(out), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+def _gpu_index(local_rank):
+    vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+    if vis:
+        ids = [v.strip() for v in vis.split(",") if v.strip()]
+        if local_rank < len(ids):
+            return ids[local_rank]
+    return local_rank
+
+
+def e2e_run(args, w, tl, torch, dist, local_rank, Lx_tile, Ly):
+    """K steps through the public worker API from a pinned host state: H2D of
+    the tile, K steps, D2H of the final tile and of the per-step metrics."""
+    host_in = torch.empty((37, Lx_tile, Ly), dtype=torch.float64, pin_memory=True)
+    host_in.copy_(w.physical_block().cpu())
+    host_out = torch.empty_like(host_in, pin_memory=True)
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier(device_ids=[local_rank])
+    t0 = time.perf_counter()
+    w.load_block(host_in)
+    for s in range(args.steps):
+        w.step(10_000_000 + s)
+    with torch.cuda.stream(w.stream):
+        host_out.copy_(w.physical_block(), non_blocking=True)
+    negatives = [m["negatives"] for m in w.metrics]  # D2H of per-step results
+    torch.cuda.synchronize()
+    el = time.perf_counter() - t0
+    if dist is not None:
+        t = torch.tensor([el], device=w.device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        el = float(t.item())
+    world = dist.get_world_size() if dist is not None else 1
+    n = Lx_tile * Ly * world * args.steps
+    nbytes = host_in.numel() * 8 * world
+    return {"value": round(n / el / 1e6, 3), "unit": "MLUPS",
+            "h2d_bytes_per_step": int(nbytes / args.steps),
+            "d2h_bytes_per_step": int((nbytes + 8 * world * args.steps) / args.steps),
+            "note": "pinned host tile -> HBM, K steps via RankWorker.step, final tile + "
+                    "per-step negatives -> host; wall clock, max over ranks",
+            "negatives_last": int(negatives[-1]) if negatives else None}
+
+
+def split_kernels(w, tl, _lib, field_desc, torch):
+    """configs[1]: propagate / bc / collide timed separately (and fused), CUDA
+    events on the launching stream, 5 reps each, on this rank's tile."""
+    lib = _lib.load()
+    g = w.geom
+    full = _lib.region(g.Hx, g.Hx + g.Lx, g.Hy, g.Hy + g.Ly)
+    st = w._status_ring[0].data_ptr()
+    sp = w.stream.cuda_stream
+    prv, nxt = field_desc(w.prv), field_desc(w.nxt)
+    tp = w.tparams
+    flags_fused = (_lib.F_WALL_BOT | _lib.F_WALL_TOP | _lib.F_CLAMP_Y | _lib.F_WRAP_X)
+    ops = {
+        "propagate": lambda: lib.tlb_propagate(prv, nxt, full, sp),
+        "bc": lambda: lib.tlb_bc(nxt, tp, 1, 1, g.Hx, g.Hx + g.Lx, st, sp),
+        "collide": lambda: lib.tlb_collide(nxt, nxt, full, tp, 0, st, sp),
+        "fused": lambda: lib.tlb_fused(prv, nxt, full, tp, flags_fused, st, sp),
+    }
+    res = {}
+    sites = g.Lx * g.Ly
+    for name, fn in ops.items():
+        ts = []
+        for _ in range(6):
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(w.stream)
+            _lib.check(fn(), name)
+            b.record(w.stream)
+            b.synchronize()
+            ts.append(a.elapsed_time(b))
+        msv = float(np.median(ts[1:]))
+        r = {"ms": round(msv, 4)}
+        if name == "bc":
+            r["gflops"] = round(FLOP_WALL_SITE * 6 * g.Lx / (msv * 1e-3) / 1e9, 1)
+            r["GBps"] = round(BYTES_SITE * 6 * g.Lx / (msv * 1e-3) / 1e9, 1)
+        else:
+            r["GBps"] = round(BYTES_SITE * sites / (msv * 1e-3) / 1e9, 1)
+            r["mlups"] = round(sites / (msv * 1e-3) / 1e6, 1)
+            if name in ("collide", "fused"):
+                r["gflops"] = round(FLOP_SITE * sites / (msv * 1e-3) / 1e9, 1)
+        res[name] = r
+    w.collect(raise_errors=False)
+    w._metrics.clear()
+    return res
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--arith", default="exact", choices=["exact", "fast"])
+    ap.add_argument("--schedule", default="overlapped", choices=["overlapped", "staged"])
+    ap.add_argument("--Lx", type=int, default=TILE_LX, help="tile Lx per GPU")
+    ap.add_argument("--Ly", type=int, default=TILE_LY)
+    ap.add_argument("--preload", type=float, default=1.0, help="s of untimed load for clocks")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-e2e", dest="e2e", action="store_false")
+    ap.add_argument("--no-split", dest="split", action="store_false")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if world != args.gpus and world > 1:
+        print(f"warning: WORLD_SIZE={world} != --gpus {args.gpus}", file=sys.stderr)
+    if args.impl == "reference":
+        return reference_arm(args, rank, world)
+    return gpu_arm(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -185,6 +185,10 @@ int tlb_pbc_self_y(const TlbField *f, tlb_stream_t stream);
 int tlb_halo_from_peers(const TlbField *f, const TlbField *left,
                         const TlbField *right, tlb_stream_t stream);
 
+/* Diagnostics: measured FP64 FMA throughput of this GPU (flop/s, 2 per
+ * DFMA), the denominator of the collide FP64 roofline. */
+int tlb_bench_dfma(int64_t iters, double *flops_per_s, tlb_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

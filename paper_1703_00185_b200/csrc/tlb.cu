@@ -739,3 +739,47 @@ int tlb_halo_from_peers(const TlbField *f, const TlbField *left, const TlbField 
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------ FP64 peak probe --
+// Independent DFMA chains (8 per thread) over a grid of 8 CTAs per SM: the
+// FP64-pipe ceiling the collide roofline is reported against (the driver's
+// MEASURED_PEAKS.json has no FP64 entry).
+__global__ void __launch_bounds__(256) k_dfma_probe(long long iters, double seed, double *sink) {
+    double a[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = seed + threadIdx.x * 1e-9 + k;
+    const double m = 0.999999999, c = 1e-9;
+    for (long long i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) a[k] = fma(a[k], m, c);
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += a[k];
+    if (s == 12345.678) sink[0] = s;  // keep the chains alive
+}
+
+extern "C" int tlb_bench_dfma(int64_t iters, double *flops_per_s, tlb_stream_t stream) {
+    int dev = 0, sms = 0;
+    TLB_CUDA_CHECK(cudaGetDevice(&dev));
+    TLB_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    double *sink = nullptr;
+    TLB_CUDA_CHECK(cudaMalloc(&sink, sizeof(double)));
+    cudaEvent_t e0, e1;
+    TLB_CUDA_CHECK(cudaEventCreate(&e0));
+    TLB_CUDA_CHECK(cudaEventCreate(&e1));
+    cudaStream_t s = (cudaStream_t)stream;
+    const int grid = sms * 8, block = 256;
+    k_dfma_probe<<<grid, block, 0, s>>>(iters / 10, 1.0, sink);  // warm-up
+    TLB_CUDA_CHECK(cudaEventRecord(e0, s));
+    k_dfma_probe<<<grid, block, 0, s>>>(iters, 1.0, sink);
+    TLB_CUDA_CHECK(cudaEventRecord(e1, s));
+    TLB_CUDA_CHECK(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    TLB_CUDA_CHECK(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(sink);
+    *flops_per_s = 2.0 * 8.0 * (double)iters * grid * block / (ms * 1e-3);
+    return TLB_OK;
+}

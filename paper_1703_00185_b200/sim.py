@@ -83,12 +83,20 @@ def _dist_rank_setup(cfg):
     return None
 
 
-def run(cfg: SimConfig) -> RunResult:
-    """Execute cfg.steps time steps on cfg.Np ranks (sim.py:62-129)."""
+def run(cfg: SimConfig, f0=None) -> RunResult:
+    """Execute cfg.steps time steps on cfg.Np ranks (sim.py:62-129).
+
+    ``f0`` (optional, an extension): a (Q, Lx, Ly) initial state -- numpy, a
+    (pinned) host tensor or a device tensor -- used instead of cfg.init."""
     torch = _lib.torch_cuda()
     vs = build_velocity_set(cfg.model)
     tiles = decompose(cfg.Lx, cfg.Ly, cfg.Np, cfg.tiling, periodic_y=cfg.periodic_y)
-    macro0 = initial_macro(cfg.init, cfg.Lx, cfg.Ly, vs, **cfg.init_kwargs)
+    macro0 = None
+    if f0 is None:
+        macro0 = initial_macro(cfg.init, cfg.Lx, cfg.Ly, vs, **cfg.init_kwargs)
+    elif tuple(f0.shape) != (vs.Q, cfg.Lx, cfg.Ly):
+        raise ConfigurationError(f"f0 has shape {tuple(f0.shape)}, expected "
+                                 f"{(vs.Q, cfg.Lx, cfg.Ly)}")
     dist = _dist_rank_setup(cfg)
     host = cfg.output == "host"
 
@@ -114,10 +122,15 @@ def run(cfg: SimConfig) -> RunResult:
                            debug_poison=cfg.debug_poison, device=dev,
                            periodic_y=cfg.periodic_y)
             sl = (slice(tile.x0, tile.x0 + tile.Lx), slice(tile.y0, tile.y0 + tile.Ly))
-            ts = [torch.as_tensor(np.ascontiguousarray(a[sl], dtype=np.float64), device=dev)
-                  for a in macro0]
-            f0 = equilibrium(*ts, vs)
-            w.load_block(f0)
+            if macro0 is not None:
+                ts = [torch.as_tensor(np.ascontiguousarray(a[sl], dtype=np.float64),
+                                      device=dev) for a in macro0]
+                w.load_block(equilibrium(*ts, vs))
+            else:
+                src = f0[:, sl[0], sl[1]]
+                if isinstance(src, np.ndarray):
+                    src = torch.from_numpy(np.ascontiguousarray(src))
+                w.load_block(src.to(dev, non_blocking=True))
             w.synchronize()
         workers.append(w)
 

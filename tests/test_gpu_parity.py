@@ -120,7 +120,10 @@ def test_fast_collide_close(vs, kern, orc):
     blk = nxt[:, 3:19, 3:19]
     out = tl.collide(blk, P(kern["params"], arith="fast"), vs)
     ref = kern["collide_0"]
-    assert np.max(np.abs(out - ref) / np.abs(ref)) < 1e-13
+    # random states are far from equilibrium, so some outputs cancel to ~0:
+    # bound the error by the site's population scale
+    scale = np.abs(ref).max(axis=0, keepdims=True)
+    assert np.max(np.abs(out - ref) / scale) < 1e-13
 
 
 # ---------------------------------------------------------- region rules --
