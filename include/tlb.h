@@ -185,6 +185,12 @@ int tlb_pbc_self_y(const TlbField *f, tlb_stream_t stream);
 int tlb_halo_from_peers(const TlbField *f, const TlbField *left,
                         const TlbField *right, tlb_stream_t stream);
 
+/* Tuning knobs (process-wide): TLB_TUNE_MINBLOCKS selects the
+ * __launch_bounds__ minimum CTAs/SM of the fused kernel (1 = compiler's
+ * choice, 4 = default, 5). */
+#define TLB_TUNE_MINBLOCKS 1
+int tlb_set_tuning(int key, int value);
+
 /* Diagnostics: measured FP64 FMA throughput of this GPU (flop/s, 2 per
  * DFMA), the denominator of the collide FP64 roofline. */
 int tlb_bench_dfma(int64_t iters, double *flops_per_s, tlb_stream_t stream);

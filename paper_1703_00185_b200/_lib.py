@@ -86,6 +86,7 @@ SIGNATURES = [
     ("tlb_pbc_self_x", _INT, [_FP, _P]),
     ("tlb_pbc_self_y", _INT, [_FP, _P]),
     ("tlb_halo_from_peers", _INT, [_FP, _FP, _FP, _P]),
+    ("tlb_set_tuning", _INT, [_INT, _INT]),
     ("tlb_bench_dfma", _INT, [_I64, ctypes.POINTER(ctypes.c_double), _P]),
 ]
 

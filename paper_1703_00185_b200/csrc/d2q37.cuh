@@ -86,6 +86,29 @@ struct Phys {
 // Defined here: the library is a single translation unit (no -rdc).
 __constant__ StencilConst C;
 
+// Population accessors: the arithmetic below reads f_l through get(l) and
+// writes results through put(l, v), so the same code runs on a
+// register-resident 37-vector (RegF) or on a shared-memory tile with the
+// results streamed straight to global memory (SmemF).
+struct RegF {
+    double (&a)[Q];
+    __device__ __forceinline__ double get(int l) const { return a[l]; }
+    __device__ __forceinline__ void put(int l, double v) { a[l] = v; }
+};
+
+struct SmemF {
+    const double *s;  // this site's column in the staged tile, stride `ss`
+    int ss;
+    double *o;        // this site's output address, population stride `os`
+    long long os;
+    unsigned neg;     // negative outputs written (count_negative)
+    __device__ __forceinline__ double get(int l) const { return s[l * ss]; }
+    __device__ __forceinline__ void put(int l, double v) {
+        o[(long long)l * os] = v;
+        neg += v < 0.0;
+    }
+};
+
 // ---------------------------------------------------------------- exact --
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
@@ -227,14 +250,13 @@ __device__ __forceinline__ double relax_exact(double f, double feq, double omega
 }
 
 // MODE 0: f <- equilibrium (bc);  MODE 1: f <- BGK relax toward equilibrium
-template <int ORDER, int MODE, int sh>
-__device__ __forceinline__ void eq_shell_apply_exact(double (&f)[Q], const EqSite &e,
-                                                     double omega) {
+template <int ORDER, int MODE, int sh, class F>
+__device__ __forceinline__ void eq_shell_apply_exact(F &f, const EqSite &e, double omega) {
     const EqShell z = eq_shell_exact<sh>(e);
     constexpr int s0 = SH_START(sh), n = SH_N(sh);
     if constexpr (sh == 0) {
         const double feq = eq_rest_exact<ORDER>(e, z);
-        f[0] = MODE ? relax_exact(f[0], feq, omega) : feq;
+        f.put(0, MODE ? relax_exact(f.get(0), feq, omega) : feq);
     } else {
 #pragma unroll
         for (int i = 0; i < n / 2; ++i) {
@@ -252,52 +274,56 @@ __device__ __forceinline__ void eq_shell_apply_exact(double (&f)[Q], const EqSit
             double fp, fm;
             eq_pair_exact<ORDER>(e, z, p, fp, fm);
             const int lm = s0 + n - 1 - i;
-            f[l] = MODE ? relax_exact(f[l], fp, omega) : fp;
-            f[lm] = MODE ? relax_exact(f[lm], fm, omega) : fm;
+            f.put(l, MODE ? relax_exact(f.get(l), fp, omega) : fp);
+            f.put(lm, MODE ? relax_exact(f.get(lm), fm, omega) : fm);
         }
     }
 }
 
-template <int ORDER, int MODE>
-__device__ __forceinline__ void eq_all_exact(double (&f)[Q], const EqSite &e, double omega) {
-    eq_shell_apply_exact<ORDER, MODE, 0>(f, e, omega);
-    eq_shell_apply_exact<ORDER, MODE, 1>(f, e, omega);
-    eq_shell_apply_exact<ORDER, MODE, 2>(f, e, omega);
-    eq_shell_apply_exact<ORDER, MODE, 3>(f, e, omega);
-    eq_shell_apply_exact<ORDER, MODE, 4>(f, e, omega);
-    eq_shell_apply_exact<ORDER, MODE, 5>(f, e, omega);
-    eq_shell_apply_exact<ORDER, MODE, 6>(f, e, omega);
-    eq_shell_apply_exact<ORDER, MODE, 7>(f, e, omega);
+template <int ORDER, int MODE, class F>
+__device__ __forceinline__ void eq_all_exact(F &f, const EqSite &e, double omega) {
+    eq_shell_apply_exact<ORDER, MODE, 0, F>(f, e, omega);
+    eq_shell_apply_exact<ORDER, MODE, 1, F>(f, e, omega);
+    eq_shell_apply_exact<ORDER, MODE, 2, F>(f, e, omega);
+    eq_shell_apply_exact<ORDER, MODE, 3, F>(f, e, omega);
+    eq_shell_apply_exact<ORDER, MODE, 4, F>(f, e, omega);
+    eq_shell_apply_exact<ORDER, MODE, 5, F>(f, e, omega);
+    eq_shell_apply_exact<ORDER, MODE, 6, F>(f, e, omega);
+    eq_shell_apply_exact<ORDER, MODE, 7, F>(f, e, omega);
 }
 
 // rho = sum_l f_l in fixed l order from +0.0 (kernels.py:49, 54; bc :198-200)
-__device__ __forceinline__ double rho_exact(const double (&f)[Q]) {
+template <class F>
+__device__ __forceinline__ double rho_exact(const F &f) {
     double rho = 0.0;
 #pragma unroll
-    for (int l = 0; l < Q; ++l) rho = dadd(rho, f[l]);
+    for (int l = 0; l < Q; ++l) rho = dadd(rho, f.get(l));
     return rho;
 }
 
-template <int l>
-__device__ __forceinline__ void mom_step(const double (&f)[Q], double &rho, double &mx,
-                                         double &my, double &e2) {
+template <int l, class F>
+__device__ __forceinline__ void mom_step(const F &f, double &rho, double &mx, double &my,
+                                         double &e2) {
     constexpr int cx = CX(l), cy = CY(l), c2 = cx * cx + cy * cy;
-    rho = dadd(rho, f[l]);
-    mx = acc_cf<cx>(mx, f[l]);
-    my = acc_cf<cy>(my, f[l]);
-    e2 = acc_cf<c2>(e2, f[l]);
+    const double fl = f.get(l);
+    rho = dadd(rho, fl);
+    mx = acc_cf<cx>(mx, fl);
+    my = acc_cf<cy>(my, fl);
+    e2 = acc_cf<c2>(e2, fl);
 }
 
 template <int... Ls>
 struct MomSeq {
-    __device__ __forceinline__ static void run(const double (&f)[Q], double &rho,
-                                               double &mx, double &my, double &e2) {
-        (mom_step<Ls>(f, rho, mx, my, e2), ...);
+    template <class F>
+    __device__ __forceinline__ static void run(const F &f, double &rho, double &mx,
+                                               double &my, double &e2) {
+        (mom_step<Ls, F>(f, rho, mx, my, e2), ...);
     }
 };
 
 // moments (kernels.py:41-71).  Returns false if !(rho > 0).
-__device__ __forceinline__ bool moments_exact(const double (&f)[Q], double &rho, double &ux,
+template <class F>
+__device__ __forceinline__ bool moments_exact(const F &f, double &rho, double &ux,
                                               double &uy, double &T) {
     double r = 0.0, mx = 0.0, my = 0.0, e2 = 0.0;
     MomSeq<0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16, 17, 18, 19, 20,
@@ -310,8 +336,8 @@ __device__ __forceinline__ bool moments_exact(const double (&f)[Q], double &rho,
 }
 
 // collide one site in place (kernels.py:139-146).  Returns TLB_ST_* bits.
-template <int ORDER>
-__device__ __forceinline__ unsigned collide_exact(double (&f)[Q], const Phys &P) {
+template <int ORDER, class F>
+__device__ __forceinline__ unsigned collide_exact(F &f, const Phys &P) {
     double rho, ux, uy, T;
     if (!moments_exact(f, rho, ux, uy, T)) return 1u;
     const double ub = dadd(ux, P.K1);
@@ -319,16 +345,16 @@ __device__ __forceinline__ unsigned collide_exact(double (&f)[Q], const Phys &P)
     const double Tb = dsub(T, P.K3);
     if (!(Tb > 0.0)) return 2u;
     const EqSite e = eq_site_exact(rho, ub, vb, Tb);
-    eq_all_exact<ORDER, 1>(f, e, P.omega);
+    eq_all_exact<ORDER, 1, F>(f, e, P.omega);
     return 0u;
 }
 
 // bc on one wall site (kernels.py:197-203): rho = sum f, f = feq(rho,0,0,Tw).
-template <int ORDER>
-__device__ __forceinline__ unsigned bc_exact(double (&f)[Q], double Tw) {
+template <int ORDER, class F>
+__device__ __forceinline__ unsigned bc_exact(F &f, double Tw) {
     const double rho = rho_exact(f);
     const EqSite e = eq_site_exact(rho, 0.0, 0.0, Tw);
-    eq_all_exact<ORDER, 0>(f, e, 0.0);
+    eq_all_exact<ORDER, 0, F>(f, e, 0.0);
     return (rho > 0.0) ? 0u : 4u;
 }
 
@@ -356,8 +382,8 @@ struct FastSite {
 // poly = A0 + A1 p + A2 p^2 + A3 p^3 + A4 p^4 with a = theta*q - s:
 // A0 = 1 + (a-2th)/2 + [a^2/8 - th*a + th^2]_{order 4}, A1 = 1 + [(a-4th)/2]_{>=3},
 // A2 = 1/2 + [(a-6th)/4]_{4}, A3 = [1/6]_{>=3}, A4 = [1/24]_{4}.
-template <int ORDER, int MODE, int sh>
-__device__ __forceinline__ void fast_shell(double (&f)[Q], const FastSite &e, double omr) {
+template <int ORDER, int MODE, int sh, class F>
+__device__ __forceinline__ void fast_shell(F &f, const FastSite &e, double omr) {
     const double q = C.qsh[sh];
     const double th = e.theta;
     const double a = fma(th, q, -e.s);
@@ -376,7 +402,7 @@ __device__ __forceinline__ void fast_shell(double (&f)[Q], const FastSite &e, do
     A0 *= W; A1 *= W; A2 *= W; A3 *= W; A4 *= W;
     constexpr int s0 = SH_START(sh), n = SH_N(sh);
     if constexpr (sh == 0) {
-        f[0] = MODE ? fma(omr, f[0], A0) : A0;
+        f.put(0, MODE ? fma(omr, f.get(0), A0) : A0);
     } else {
 #pragma unroll
         for (int i = 0; i < n / 2; ++i) {
@@ -394,38 +420,39 @@ __device__ __forceinline__ void fast_shell(double (&f)[Q], const FastSite &e, do
             const double ev = fma(p2, fma(p2, A4, A2), A0);
             const double od = p * fma(p2, A3, A1);
             if (MODE) {
-                f[l] = fma(omr, f[l], ev + od);
-                f[lm] = fma(omr, f[lm], ev - od);
+                f.put(l, fma(omr, f.get(l), ev + od));
+                f.put(lm, fma(omr, f.get(lm), ev - od));
             } else {
-                f[l] = ev + od;
-                f[lm] = ev - od;
+                f.put(l, ev + od);
+                f.put(lm, ev - od);
             }
         }
     }
 }
 
-template <int ORDER, int MODE>
-__device__ __forceinline__ void fast_all(double (&f)[Q], const FastSite &e, double omr) {
-    fast_shell<ORDER, MODE, 0>(f, e, omr);
-    fast_shell<ORDER, MODE, 1>(f, e, omr);
-    fast_shell<ORDER, MODE, 2>(f, e, omr);
-    fast_shell<ORDER, MODE, 3>(f, e, omr);
-    fast_shell<ORDER, MODE, 4>(f, e, omr);
-    fast_shell<ORDER, MODE, 5>(f, e, omr);
-    fast_shell<ORDER, MODE, 6>(f, e, omr);
-    fast_shell<ORDER, MODE, 7>(f, e, omr);
+template <int ORDER, int MODE, class F>
+__device__ __forceinline__ void fast_all(F &f, const FastSite &e, double omr) {
+    fast_shell<ORDER, MODE, 0, F>(f, e, omr);
+    fast_shell<ORDER, MODE, 1, F>(f, e, omr);
+    fast_shell<ORDER, MODE, 2, F>(f, e, omr);
+    fast_shell<ORDER, MODE, 3, F>(f, e, omr);
+    fast_shell<ORDER, MODE, 4, F>(f, e, omr);
+    fast_shell<ORDER, MODE, 5, F>(f, e, omr);
+    fast_shell<ORDER, MODE, 6, F>(f, e, omr);
+    fast_shell<ORDER, MODE, 7, F>(f, e, omr);
 }
 
-template <int ORDER>
-__device__ __forceinline__ unsigned collide_fast(double (&f)[Q], const Phys &P) {
+template <int ORDER, class F>
+__device__ __forceinline__ unsigned collide_fast(F &f, const Phys &P) {
     double r0 = 0.0, r1 = 0.0, mx = 0.0, my = 0.0, e2 = 0.0;
 #pragma unroll
     for (int l = 0; l < Q; ++l) {
-        if (l & 1) r1 += f[l]; else r0 += f[l];
-        if (CX(l)) mx = fma((double)CX(l), f[l], mx);
-        if (CY(l)) my = fma((double)CY(l), f[l], my);
+        const double fl = f.get(l);
+        if (l & 1) r1 += fl; else r0 += fl;
+        if (CX(l)) mx = fma((double)CX(l), fl, mx);
+        if (CY(l)) my = fma((double)CY(l), fl, my);
         if (CX(l) * CX(l) + CY(l) * CY(l))
-            e2 = fma((double)(CX(l) * CX(l) + CY(l) * CY(l)), f[l], e2);
+            e2 = fma((double)(CX(l) * CX(l) + CY(l) * CY(l)), fl, e2);
     }
     const double rho = r0 + r1;
     if (!(rho > 0.0)) return 1u;
@@ -440,23 +467,24 @@ __device__ __forceinline__ unsigned collide_fast(double (&f)[Q], const Phys &P) 
     e.theta = fma(Tb, C.rcs2, -1.0);
     e.s = fma(e.vx, e.vx, e.vy * e.vy);
     e.W = P.omega * rho;
-    fast_all<ORDER, 1>(f, e, 1.0 - P.omega);
+    fast_all<ORDER, 1, F>(f, e, 1.0 - P.omega);
     return 0u;
 }
 
-template <int ORDER>
-__device__ __forceinline__ unsigned bc_fast(double (&f)[Q], double Tw) {
+template <int ORDER, class F>
+__device__ __forceinline__ unsigned bc_fast(F &f, double Tw) {
     double r0 = 0.0, r1 = 0.0;
 #pragma unroll
     for (int l = 0; l < Q; ++l) {
-        if (l & 1) r1 += f[l]; else r0 += f[l];
+        const double fl = f.get(l);
+        if (l & 1) r1 += fl; else r0 += fl;
     }
     const double rho = r0 + r1;
     FastSite e;
     e.vx = 0.0; e.vy = 0.0; e.s = 0.0;
     e.theta = fma(Tw, C.rcs2, -1.0);
     e.W = rho;
-    fast_all<ORDER, 0>(f, e, 0.0);
+    fast_all<ORDER, 0, F>(f, e, 0.0);
     return (rho > 0.0) ? 0u : 4u;
 }
 

@@ -48,6 +48,7 @@ static int launch_check(const char *what) {
 }
 
 static bool g_stencil_set[64];
+static int g_minb = 4;  // tuning: __launch_bounds__ min blocks of the fused kernel
 
 // --------------------------------------------------------- device helpers --
 struct Fld {
@@ -78,10 +79,21 @@ static Phys mkphys(const TlbParams *p) {
     return P;
 }
 
+// A launch covers an interior rectangle (plain gather: no halo remapping,
+// no wall rows -- the hot path) plus up to four frame rectangles (implicit
+// halos, bc rows).  Frame blocks get the LOW block indices so their few
+// slow sites overlap the interior stream instead of forming a tail.
+struct Rect {
+    int x0, y0, ny;
+    unsigned n;  // sites
+};
+
 struct SiteLaunch {
     Fld src, dst;
-    int x0, y0, ny;
-    long long nsites;
+    Rect in;
+    Rect fr[4];
+    unsigned fr_end[4];  // prefix sums of frame sites
+    unsigned nfb;        // frame blocks
     int bot_lo, bot_hi, top_lo, top_hi;  // bc rows (padded y), empty if lo>=hi
     int flags;
     Phys P;
@@ -102,14 +114,29 @@ __device__ __forceinline__ void report(TlbStatus *st, unsigned bits, int x, int 
     }
 }
 
+// Block-level count of negative populations: one atomic per CTA that saw
+// any (count_negative, monitoring only).
+__device__ __forceinline__ void count_neg_n(TlbStatus *st, unsigned n) {
+    n = __reduce_add_sync(0xffffffffu, n);
+    if (__syncthreads_or(n != 0)) {
+        __shared__ unsigned warp_n[32];
+        if ((threadIdx.x & 31) == 0) warp_n[threadIdx.x >> 5] = n;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned t = 0;
+            for (unsigned w = 0; w < (blockDim.x + 31) / 32; ++w) t += warp_n[w];
+            if (t) atomicAdd(&st->negatives, (unsigned long long)t);
+        }
+    }
+}
+
 __device__ __forceinline__ void count_neg(TlbStatus *st, const double (&f)[Q], bool active) {
     unsigned n = 0;
     if (active) {
 #pragma unroll
         for (int l = 0; l < Q; ++l) n += f[l] < 0.0;
     }
-    n = __reduce_add_sync(0xffffffffu, n);
-    if ((threadIdx.x & 31) == 0 && n) atomicAdd(&st->negatives, (unsigned long long)n);
+    count_neg_n(st, n);
 }
 
 enum Kind { K_PROPAGATE = 0, K_BC = 1, K_COLLIDE = 2, K_FUSED = 3 };
@@ -181,33 +208,57 @@ __device__ __forceinline__ void load_inplace(double (&f)[Q], const Fld &s, int x
     for (int l = 0; l < Q; ++l) f[l] = p[(long long)l * s.sl];
 }
 
-// One thread = one site.  Sites are enumerated y-fastest over the region so
-// consecutive lanes touch consecutive addresses of every population plane.
-template <int KIND, bool EXACT, int ORDER, bool INPLACE>
-__global__ void __launch_bounds__(128) k_site(SiteLaunch L) {
-    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    const bool active = i < L.nsites;
-    const long long ii = active ? i : L.nsites - 1;
-    const int x = L.x0 + (int)(ii / L.ny);
-    const int y = L.y0 + (int)(ii % L.ny);
+template <int l>
+__device__ __forceinline__ void load_plain_one(double (&f)[Q], const Fld &s, long long site,
+                                               bool gather) {
+    long long off = site + (long long)l * s.sl;
+    if (gather) off -= (long long)CX(l) * s.sx + (long long)CY(l) * s.sy;
+    f[l] = __ldg(s.base + off);
+}
+
+template <int... Ls>
+struct PlainSeq {
+    __device__ __forceinline__ static void run(double (&f)[Q], const Fld &s, long long site,
+                                               bool gather) {
+        (load_plain_one<Ls>(f, s, site, gather), ...);
+    }
+};
+
+// Interior loads: one 64-bit site offset plus compile-time population
+// offsets -- no branches, all 37 loads issued back to back.
+__device__ __forceinline__ void load_plain(double (&f)[Q], const Fld &s, int x, int y,
+                                           bool gather) {
+    const long long site = (long long)x * s.sx + (long long)y * s.sy;
+    PlainSeq<0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16, 17, 18, 19, 20, 21,
+             22, 23, 24, 25, 26, 27, 28, 29, 30, 31, 32, 33, 34, 35, 36>::run(f, s, site, gather);
+}
+
+template <int KIND, bool EXACT, int ORDER, bool INPLACE, bool EDGE>
+__device__ __forceinline__ void site_body(const SiteLaunch &L, int x, int y, bool active) {
     double f[Q];
-    const bool gather = KIND == K_PROPAGATE || KIND == K_FUSED;
-    const bool implicit = (L.flags & (TLB_F_WRAP_X | TLB_F_WRAP_Y | TLB_F_CLAMP_Y)) != 0;
-    if (INPLACE)
+    constexpr bool gather = KIND == K_PROPAGATE || KIND == K_FUSED;
+    if (INPLACE) {
         load_inplace(f, L.src, x, y);
-    else
+    } else if (EDGE) {
+        const bool implicit = (L.flags & (TLB_F_WRAP_X | TLB_F_WRAP_Y | TLB_F_CLAMP_Y)) != 0;
         load_all(f, L.src, x, y, gather, implicit, L.flags);
+    } else {
+        load_plain(f, L.src, x, y, gather);
+    }
     unsigned bits = 0;
-    if (KIND == K_BC || KIND == K_FUSED) {
+    if (EDGE && (KIND == K_BC || KIND == K_FUSED)) {
         const bool bot = y >= L.bot_lo && y < L.bot_hi;
         const bool top = y >= L.top_lo && y < L.top_hi;
         if (bot || top) {
             const double Tw = bot ? L.P.Tbot : L.P.Ttop;
-            bits |= EXACT ? bc_exact<ORDER>(f, Tw) : bc_fast<ORDER>(f, Tw);
+            RegF rf{f};
+            bits |= EXACT ? bc_exact<ORDER>(rf, Tw) : bc_fast<ORDER>(rf, Tw);
         }
     }
-    if (KIND == K_COLLIDE || KIND == K_FUSED)
-        bits |= EXACT ? collide_exact<ORDER>(f, L.P) : collide_fast<ORDER>(f, L.P);
+    if (KIND == K_COLLIDE || KIND == K_FUSED) {
+        RegF rf{f};
+        bits |= EXACT ? collide_exact<ORDER>(rf, L.P) : collide_fast<ORDER>(rf, L.P);
+    }
     if (active) {
         report(L.status, bits, x, y, L.step);
         store_all(f, L.dst, x, y);
@@ -215,15 +266,56 @@ __global__ void __launch_bounds__(128) k_site(SiteLaunch L) {
     if (L.flags & TLB_F_COUNT_NEG) count_neg(L.status, f, active);
 }
 
+// One thread = one site.  Sites are enumerated y-fastest inside each
+// rectangle so consecutive lanes touch consecutive addresses of every
+// population plane.
+template <int KIND, bool EXACT, int ORDER, bool INPLACE, int MINB>
+__global__ void __launch_bounds__(128, MINB) k_site(SiteLaunch L) {
+    if (blockIdx.x < L.nfb) {
+        const unsigned total = L.fr_end[3];
+        const unsigned i = blockIdx.x * blockDim.x + threadIdx.x;
+        const bool active = i < total;
+        const unsigned ii = active ? i : total - 1;
+        const int r = ii < L.fr_end[0] ? 0 : ii < L.fr_end[1] ? 1 : ii < L.fr_end[2] ? 2 : 3;
+        const unsigned loc = ii - (r ? L.fr_end[r - 1] : 0u);
+        const Rect &R = L.fr[r];
+        site_body<KIND, EXACT, ORDER, INPLACE, true>(L, R.x0 + (int)(loc / R.ny),
+                                                     R.y0 + (int)(loc % R.ny), active);
+    } else {
+        const unsigned i = (blockIdx.x - L.nfb) * blockDim.x + threadIdx.x;
+        const bool active = i < L.in.n;
+        const unsigned ii = active ? i : L.in.n - 1;
+        site_body<KIND, EXACT, ORDER, INPLACE, false>(L, L.in.x0 + (int)(ii / L.in.ny),
+                                                      L.in.y0 + (int)(ii % L.in.ny), active);
+    }
+}
+
 // --------------------------------------------------------------- launcher --
 template <int KIND, bool INPLACE>
 static int launch_site(SiteLaunch &L, bool exact, int order, cudaStream_t s, const char *what) {
-    if (L.nsites <= 0) return TLB_OK;
     const int bs = 128;
-    const long long nb = (L.nsites + bs - 1) / bs;
-    if (nb > 0x7fffffffLL) return fail(TLB_ERR_CONTRACT, "%s: region too large", what);
+    const unsigned long long nf = L.fr_end[3];
+    L.nfb = (unsigned)((nf + bs - 1) / bs);
+    const unsigned long long nb = L.nfb + (L.in.n + (unsigned long long)bs - 1) / bs;
+    if (nb == 0) return TLB_OK;
+    if (nb > 0x7fffffffULL) return fail(TLB_ERR_CONTRACT, "%s: region too large", what);
     dim3 grid((unsigned)nb), block(bs);
-#define TLB_L(E, O) k_site<KIND, E, O, INPLACE><<<grid, block, 0, s>>>(L)
+// 4 CTAs of 128 threads per SM (<= 128 registers): measured best for both
+// arithmetic modes (profiles/r01_variants.md); 1 and 5 stay as tuning knobs.
+#define TLB_L(E, O) k_site<KIND, E, O, INPLACE, 4><<<grid, block, 0, s>>>(L)
+#define TLB_LT(E, O)                                                               \
+    do {                                                                           \
+        if (g_minb == 1) k_site<KIND, E, O, INPLACE, 1><<<grid, block, 0, s>>>(L); \
+        else if (g_minb == 5) k_site<KIND, E, O, INPLACE, 5><<<grid, block, 0, s>>>(L); \
+        else TLB_L(E, O);                                                          \
+    } while (0)
+    if constexpr (KIND == K_FUSED) {
+        if (order == 4) {
+            if (exact) TLB_LT(true, 4);
+            else TLB_LT(false, 4);
+            return launch_check(what);
+        }
+    }
     if (exact) {
         if (order == 4) TLB_L(true, 4);
         else if (order == 3) TLB_L(true, 3);
@@ -234,6 +326,7 @@ static int launch_site(SiteLaunch &L, bool exact, int order, cudaStream_t s, con
         else TLB_L(false, 2);
     }
 #undef TLB_L
+#undef TLB_LT
     return launch_check(what);
 }
 
@@ -261,13 +354,60 @@ static int check_region(const TlbField *f, TlbRegion r, const char *what) {
     return TLB_OK;
 }
 
+static Rect mkrect(int x0, int x1, int y0, int y1) {
+    Rect R;
+    R.x0 = x0;
+    R.y0 = y0;
+    const long long nx = x1 > x0 ? x1 - x0 : 0, ny = y1 > y0 ? y1 - y0 : 0;
+    R.ny = ny > 0 ? (int)ny : 1;
+    R.n = (unsigned)(nx * ny);
+    return R;
+}
+
+static void set_frames(SiteLaunch &L, const Rect *rs, int n) {
+    unsigned acc = 0;
+    for (int k = 0; k < 4; ++k) {
+        L.fr[k] = k < n ? rs[k] : mkrect(0, 0, 0, 0);
+        acc += L.fr[k].n;
+        L.fr_end[k] = acc;
+    }
+}
+
+// Whole region on the plain (interior) path.
 static void fill_region(SiteLaunch &L, TlbRegion r) {
-    L.x0 = r.x0;
-    L.y0 = r.y0;
-    L.ny = r.y1 > r.y0 ? r.y1 - r.y0 : 0;
-    const long long nx = r.x1 > r.x0 ? r.x1 - r.x0 : 0;
-    L.nsites = nx * L.ny;
-    if (L.ny == 0) L.ny = 1;
+    L.in = mkrect(r.x0, r.x1, r.y0, r.y1);
+    set_frames(L, nullptr, 0);
+}
+
+// Whole region on the edge path (bc launches).
+static void fill_region_edge(SiteLaunch &L, TlbRegion r) {
+    L.in = mkrect(0, 0, 0, 0);
+    Rect R = mkrect(r.x0, r.x1, r.y0, r.y1);
+    set_frames(L, &R, 1);
+}
+
+// Split r into the interior rectangle that needs no halo remapping and no
+// bc, and the frame bands around it (RankWorker._frame_slices,
+// runtime.py:326-338, generalised to the flags).
+static void split_region(SiteLaunch &L, TlbRegion r, const TlbField *f, int flags) {
+    int px0 = r.x0, px1 = r.x1, py0 = r.y0, py1 = r.y1;
+    const int h = TLB_WALL_ROWS;  // == max hop
+    if (flags & TLB_F_WRAP_X) {
+        px0 = px0 > f->Hx + h ? px0 : f->Hx + h;
+        px1 = px1 < f->Hx + f->Lx - h ? px1 : f->Hx + f->Lx - h;
+    }
+    if (flags & (TLB_F_WRAP_Y | TLB_F_CLAMP_Y | TLB_F_WALL_BOT | TLB_F_WALL_TOP)) {
+        py0 = py0 > f->Hy + h ? py0 : f->Hy + h;
+        py1 = py1 < f->Hy + f->Ly - h ? py1 : f->Hy + f->Ly - h;
+    }
+    if (px1 <= px0 || py1 <= py0) {
+        fill_region_edge(L, r);
+        return;
+    }
+    L.in = mkrect(px0, px1, py0, py1);
+    Rect rs[4] = {mkrect(r.x0, r.x1, r.y0, py0), mkrect(r.x0, r.x1, py1, r.y1),
+                  mkrect(r.x0, px0, py0, py1), mkrect(px1, r.x1, py0, py1)};
+    set_frames(L, rs, 4);
 }
 
 static void wall_rows(SiteLaunch &L, const TlbField *f, int flags) {
@@ -412,7 +552,8 @@ __global__ void k_moments(Fld f, int x0, int y0, int ny, long long n, double *rh
 #pragma unroll
     for (int l = 0; l < Q; ++l) fl[l] = p[(long long)l * f.sl];
     double r, u, v, t;
-    bool ok = moments_exact(fl, r, u, v, t);
+    RegF rf{fl};
+    bool ok = moments_exact(rf, r, u, v, t);
     const long long o = (long long)xi * ld + yi;
     rho[o] = r; ux[o] = u; uy[o] = v; T[o] = t;
     if (check && !ok) report(st, 1u, x0 + xi, y0 + yi, -1);
@@ -429,9 +570,10 @@ __global__ void k_equilibrium(const double *rho, const double *ux, const double 
     double f[Q];
 #pragma unroll
     for (int l = 0; l < Q; ++l) f[l] = 0.0;
+    RegF rf{f};
     if (EXACT) {
         const EqSite e = eq_site_exact(r, u, v, t);
-        eq_all_exact<ORDER, 0>(f, e, 0.0);
+        eq_all_exact<ORDER, 0>(rf, e, 0.0);
     } else {
         FastSite e;
         e.vx = u * C.rcs;
@@ -439,7 +581,7 @@ __global__ void k_equilibrium(const double *rho, const double *ux, const double 
         e.theta = fma(t, C.rcs2, -1.0);
         e.s = fma(e.vx, e.vx, e.vy * e.vy);
         e.W = r;
-        fast_all<ORDER, 0>(f, e, 0.0);
+        fast_all<ORDER, 0>(rf, e, 0.0);
     }
 #pragma unroll
     for (int l = 0; l < Q; ++l) out[(long long)l * ld + i] = f[l];
@@ -473,6 +615,16 @@ __global__ void k_count_negative(Fld f, int x0, int y0, int ny, long long n, Tlb
 extern "C" {
 
 int tlb_version(void) { return 1; }
+
+int tlb_set_tuning(int key, int value) {
+    if (key == TLB_TUNE_MINBLOCKS) {
+        if (value != 1 && value != 4 && value != 5)
+            return fail(TLB_ERR_CONTRACT, "min blocks must be 1, 4 or 5");
+        g_minb = value;
+        return TLB_OK;
+    }
+    return fail(TLB_ERR_CONTRACT, "unknown tuning key %d", key);
+}
 
 const char *tlb_last_error(void) { return g_msg.c_str(); }
 
@@ -566,7 +718,7 @@ int tlb_bc(const TlbField *f, const TlbParams *p, int top, int bottom, int32_t x
         if (side == 0) { S.top_lo = S.top_hi = 0; }
         else { S.bot_lo = S.bot_hi = 0; }
         TlbRegion r = {x0, x1, side == 0 ? S.bot_lo : S.top_lo, side == 0 ? S.bot_hi : S.top_hi};
-        fill_region(S, r);
+        fill_region_edge(S, r);
         if ((e = launch_site<K_BC, true>(S, p->arith == TLB_ARITH_EXACT, p->order,
                                          (cudaStream_t)stream, "bc")))
             return e;
@@ -618,7 +770,7 @@ int tlb_fused(const TlbField *prv, const TlbField *nxt, TlbRegion r, const TlbPa
     L.flags = flags;
     L.step = -1;
     wall_rows(L, prv, flags);
-    fill_region(L, r);
+    split_region(L, r, prv, flags);
     return launch_site<K_FUSED, false>(L, p->arith == TLB_ARITH_EXACT, p->order,
                                        (cudaStream_t)stream, "fused");
 }

@@ -57,6 +57,16 @@ def main():
         "fused_fast_plain": lambda: lib.tlb_fused(P, N, full, fa, 0, st.ptr, s),
         "fused_fast_step": lambda: lib.tlb_fused(P, N, full, fa, W | IMP, st.ptr, s),
     }
+    def tuned(fn, key, val, default):
+        def run():
+            lib.tlb_set_tuning(key, val)
+            r = fn()
+            lib.tlb_set_tuning(key, default)
+            return r
+        return run
+    for mb in (1, 5):
+        variants[f"fused_exact_step_neg_minb{mb}"] = tuned(variants["fused_exact_step_neg"], 1, mb, 4)
+        variants[f"fused_fast_step_minb{mb}"] = tuned(variants["fused_fast_step"], 1, mb, 4)
     sites = a.Lx * a.Ly
     out = {}
     for name, fn in variants.items():
