@@ -70,7 +70,7 @@ def main():
     sites = a.Lx * a.Ly
     out = {}
     for name, fn in variants.items():
-        if a.only and a.only not in name:
+        if a.only and name not in a.only.split(","):
             continue
         ts = []
         for _ in range(a.reps + 1):
