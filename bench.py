@@ -215,7 +215,9 @@ def gpu_arm(args, rank, world, local_rank):
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(w.stream)
+    th0 = time.perf_counter()
     run_steps(args.steps, s)
+    host_ms = (time.perf_counter() - th0) * 1e3 / args.steps
     e1.record(w.stream)
     torch.cuda.synchronize()
     barrier()
@@ -276,7 +278,8 @@ def gpu_arm(args, rank, world, local_rank):
                                   "frac": round(kern_tflops / fp64_peak, 4),
                                   "flops_per_site": FLOP_SITE}},
             "clocks": clocks,
-            "gpu_launches": args.steps * (1 if world == 1 else 7),
+            "host_enqueue_ms_per_step": round(host_ms, 4),
+            "gpu_launches": args.steps * (1 if world == 1 else 4),
         }
         if split:
             out["split"] = split

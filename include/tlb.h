@@ -185,6 +185,33 @@ int tlb_pbc_self_y(const TlbField *f, tlb_stream_t stream);
 int tlb_halo_from_peers(const TlbField *f, const TlbField *left,
                         const TlbField *right, tlb_stream_t stream);
 
+/* ---- 1-D X ring across GPUs (one process per GPU) ----------------------
+ * Replaces Fabric + pbc_c + the overlapped RankWorker.step for ranks on
+ * different GPUs (runtime.py:116-160, 269-284, 378-396).  NCCL is loaded at
+ * run time (libnccl.so.2 -- the copy PyTorch already loaded, if any). */
+typedef struct TlbRing *tlb_ring_t;
+
+int tlb_nccl_version(int *version);
+/* 128-byte ncclUniqueId, created on rank 0 and broadcast by the caller */
+int tlb_nccl_unique_id(char *out128);
+/* left = rank-1, right = rank+1 (mod nranks), runtime.py:76-77 */
+int tlb_ring_create(const char *uid128, int nranks, int rank, int device,
+                    tlb_ring_t *out);
+int tlb_ring_destroy(tlb_ring_t ring);
+/* pack both X faces of f (ymode as tlb_pack_x), exchange with the ring
+ * neighbours, unpack into the X halo columns; sbuf/rbuf hold 2 payloads
+ * (tlb_face_payload_len each, +x face first). */
+int tlb_ring_exchange(tlb_ring_t ring, const TlbField *f, int ymode,
+                      double *sbuf, double *rbuf, tlb_stream_t stream);
+/* One overlapped time step: pack -> NCCL exchange (side stream) || bulk
+ * fused kernel (stream) -> unpack + border columns (side stream) -> join.
+ * flags as tlb_fused without TLB_F_WRAP_X.  ev_bulk0/1 (cudaEvent_t or NULL)
+ * are recorded around the bulk kernel on `stream`. */
+int tlb_ring_step(tlb_ring_t ring, const TlbField *prv, const TlbField *nxt,
+                  const TlbParams *p, int flags, TlbStatus *status,
+                  double *sbuf, double *rbuf, void *ev_bulk0, void *ev_bulk1,
+                  tlb_stream_t stream);
+
 /* Tuning knobs (process-wide): TLB_TUNE_MINBLOCKS selects the
  * __launch_bounds__ minimum CTAs/SM of the fused kernel (1 = compiler's
  * choice, 4 = default, 5). */

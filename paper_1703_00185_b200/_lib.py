@@ -86,6 +86,12 @@ SIGNATURES = [
     ("tlb_pbc_self_x", _INT, [_FP, _P]),
     ("tlb_pbc_self_y", _INT, [_FP, _P]),
     ("tlb_halo_from_peers", _INT, [_FP, _FP, _FP, _P]),
+    ("tlb_nccl_version", _INT, [ctypes.POINTER(_INT)]),
+    ("tlb_nccl_unique_id", _INT, [ctypes.c_char_p]),
+    ("tlb_ring_create", _INT, [ctypes.c_char_p, _INT, _INT, _INT, ctypes.POINTER(_P)]),
+    ("tlb_ring_destroy", _INT, [_P]),
+    ("tlb_ring_exchange", _INT, [_P, _FP, _INT, _P, _P, _P]),
+    ("tlb_ring_step", _INT, [_P, _FP, _FP, _PP, _INT, _P, _P, _P, _P, _P, _P]),
     ("tlb_set_tuning", _INT, [_INT, _INT]),
     ("tlb_bench_dfma", _INT, [_I64, ctypes.POINTER(ctypes.c_double), _P]),
 ]

@@ -935,3 +935,6 @@ extern "C" int tlb_bench_dfma(int64_t iters, double *flops_per_s, tlb_stream_t s
     *flops_per_s = 2.0 * 8.0 * (double)iters * grid * block / (ms * 1e-3);
     return TLB_OK;
 }
+
+// 1-D X ring across GPUs (NCCL), same translation unit
+#include "tlb_ring.cuh"

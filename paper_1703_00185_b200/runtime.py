@@ -176,8 +176,9 @@ class Fabric:
         self.send(w.tile.rank, nb["left"], "x-", step, out_minus, ev)
         return step
 
-    def finish_x(self, w, handle, in_plus, in_minus):
+    def finish_x(self, w, handle, in_plus, in_minus, stream=None):
         torch = _lib.torch_cuda()
+        stream = stream or w.stream
         step = handle
         nb = w.tile.neighbors
         for tag, src, dst in (("x+", nb["left"], in_plus), ("x-", nb["right"], in_minus)):
@@ -185,20 +186,25 @@ class Fabric:
             if payload.numel() != dst.numel():
                 raise ProtocolError(f"rank {w.tile.rank}: X payload size mismatch")
             if ev is not None:
-                w.stream.wait_event(ev)
-            with torch.cuda.stream(w.stream):
+                stream.wait_event(ev)
+            with torch.cuda.stream(stream):
                 dst.copy_(payload, non_blocking=True)
             if payload.device == dst.device:
-                payload.record_stream(w.stream)
+                payload.record_stream(stream)
             else:
                 w.retain(payload)  # peer copy: keep alive until the next sync
 
 
 class DistFabric:
-    """X-face exchange between processes with torch.distributed
-    point-to-point (NCCL over NVLink on B200s; gloo in the CPU tests).
-    The four transfers of a step are one batched group, issued on the rank's
-    communication stream so they overlap the bulk kernel."""
+    """X-face exchange between processes (one per GPU).
+
+    With an NCCL process group the exchange is native: ``ring()`` builds a
+    libtlb ``TlbRing`` (its own NCCL communicator over NVLink, unique id
+    broadcast through torch.distributed) and RankWorker enqueues whole steps
+    through ``tlb_ring_step`` -- pack, grouped send/recv on a high-priority
+    side stream, bulk kernel, unpack and border kernel in one C call.
+    ``start_x``/``finish_x`` (torch.distributed batched point-to-point) carry
+    the same payloads for other backends; the CPU tests run them over gloo."""
 
     def __init__(self, group=None, timeout=60.0):
         import torch.distributed as dist
@@ -206,8 +212,35 @@ class DistFabric:
         self.group = group
         self.timeout = timeout
         self.Np = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
         self.abort = threading.Event()
         self.failures = []
+        self._ring = None
+
+    @property
+    def native(self):
+        return self.dist.get_backend(self.group) == "nccl"
+
+    def ring(self, device_index):
+        """The libtlb NCCL ring for this process (created on first use)."""
+        if self._ring is None:
+            import ctypes
+            lib = _lib.load()
+            uid = ctypes.create_string_buffer(128)
+            if self.rank == 0:
+                _lib.check(lib.tlb_nccl_unique_id(uid), "nccl unique id")
+            obj = [bytes(uid.raw)]
+            self.dist.broadcast_object_list(obj, src=0, group=self.group)
+            h = ctypes.c_void_p()
+            _lib.check(lib.tlb_ring_create(obj[0], self.Np, self.rank, int(device_index),
+                                           ctypes.byref(h)), "ring create")
+            self._ring = h
+        return self._ring
+
+    def close(self):
+        if self._ring is not None:
+            _lib.load().tlb_ring_destroy(self._ring)
+            self._ring = None
 
     def start_x(self, w, step, out_plus, out_minus):
         dist = self.dist
@@ -218,7 +251,8 @@ class DistFabric:
                dist.P2POp(dist.irecv, w.rbuf_minus, nb["right"], self.group)]
         return dist.batch_isend_irecv(ops)
 
-    def finish_x(self, w, handle, in_plus, in_minus):
+    def finish_x(self, w, handle, in_plus, in_minus, stream=None):
+        # called under torch.cuda.stream(stream): wait() orders it after NCCL
         for req in handle:
             try:
                 req.wait()
@@ -273,11 +307,16 @@ class RankWorker:
             _lib.ensure_stencil(vs, self.device.index)
             self.prv, self.nxt = allocate_field(self.geom, vs, device=self.device)
             self.stream = torch.cuda.Stream(self.device)
-            self.comm_stream = torch.cuda.Stream(self.device)
+            self.comm_stream = torch.cuda.Stream(self.device, priority=-1)
             n = int(_lib.load().tlb_face_payload_len(field_desc(self.prv)))
             self.payload_len = n
             self.rbuf_plus = torch.empty(n, dtype=torch.float64, device=self.device)
             self.rbuf_minus = torch.empty(n, dtype=torch.float64, device=self.device)
+            self._ring = None
+            if isinstance(fabric, DistFabric) and fabric.native and tile.grid[0] > 1:
+                self._ring = fabric.ring(self.device.index)
+                self.sbuf2 = torch.empty(2 * n, dtype=torch.float64, device=self.device)
+                self.rbuf2 = torch.empty(2 * n, dtype=torch.float64, device=self.device)
             self._status_ring = torch.zeros((self._RING, _lib.STATUS_BYTES),
                                             dtype=torch.uint8, device=self.device)
             # order the allocations' zero-fills before any work on our stream
@@ -339,15 +378,16 @@ class RankWorker:
                                            buf.data_ptr(), self._sp()), "pack_x")
         return buf
 
-    def unpack_x(self, f, sign, payload):
+    def unpack_x(self, f, sign, payload, stream=None):
         """Scatter a received X payload into the halo columns (runtime.py:210-224)."""
         torch = _lib.torch_cuda()
         if not isinstance(payload, torch.Tensor):
             payload = torch.as_tensor(np.asarray(payload, dtype=np.float64), device=self.device)
         if payload.numel() != self.payload_len:
             raise ProtocolError(f"rank {self.tile.rank}: X payload size mismatch")
+        sp = (stream or self.stream).cuda_stream
         self._check(_lib.load().tlb_unpack_x(field_desc(f), int(sign), payload.data_ptr(),
-                                             self._sp()), "unpack_x")
+                                             sp), "unpack_x")
 
     def pbc_c(self, f, step):
         """Exchange the X halo columns around the ring (runtime.py:281-284)."""
@@ -362,12 +402,13 @@ class RankWorker:
         with torch.cuda.stream(self.stream):
             return self.fabric.start_x(self, step, out_plus, out_minus)
 
-    def _finish_exchange(self, f, handle):
+    def _finish_exchange(self, f, handle, stream=None):
         torch = _lib.torch_cuda()
-        with torch.cuda.stream(self.stream):
-            self.fabric.finish_x(self, handle, self.rbuf_plus, self.rbuf_minus)
-        self.unpack_x(f, 1, self.rbuf_plus)
-        self.unpack_x(f, -1, self.rbuf_minus)
+        stream = stream or self.stream
+        with torch.cuda.stream(stream):
+            self.fabric.finish_x(self, handle, self.rbuf_plus, self.rbuf_minus, stream)
+        self.unpack_x(f, 1, self.rbuf_plus, stream)
+        self.unpack_x(f, -1, self.rbuf_minus, stream)
 
     def _extend_wall_halos(self, f):
         """runtime.py:296-305."""
@@ -398,14 +439,14 @@ class RankWorker:
         return rows
 
     # -- schedules -----------------------------------------------------------
-    def _fused(self, x0, x1, flags, st):
+    def _fused(self, x0, x1, flags, st, stream=None):
         g = self.geom
         if x1 <= x0:
             return
+        sp = (stream or self.stream).cuda_stream
         self._check(_lib.load().tlb_fused(
             field_desc(self.prv), field_desc(self.nxt),
-            _lib.region(x0, x1, g.Hy, g.Hy + g.Ly), self.tparams, flags, st,
-            self._sp()), "fused")
+            _lib.region(x0, x1, g.Hy, g.Hy + g.Ly), self.tparams, flags, st, sp), "fused")
 
     def step(self, step_no):
         """One time step (runtime.py:355-400), enqueued on the rank's stream."""
@@ -432,6 +473,11 @@ class RankWorker:
             if self.self_ring:
                 self._check(lib.tlb_pbc_self_x(field_desc(self.prv), self._sp()), "pbc_c")
                 self._handle = None
+            elif self._ring is not None:
+                self._check(lib.tlb_ring_exchange(
+                    self._ring, field_desc(self.prv), 0, self.sbuf2.data_ptr(),
+                    self.rbuf2.data_ptr(), self._sp()), "ring exchange")
+                self._handle = None
             else:
                 self._handle = self._start_exchange(step_no, self.pack_x(self.prv, 1),
                                                     self.pack_x(self.prv, -1))
@@ -452,6 +498,15 @@ class RankWorker:
                 flags | _lib.F_WRAP_X, st, self._sp()), "fused")
             self._handle = None
             return
+        if self._ring is not None:
+            ev[1].record(self.stream)
+            ev[2].record(self.stream)
+            self._check(lib.tlb_ring_step(
+                self._ring, field_desc(self.prv), field_desc(self.nxt), self.tparams, flags,
+                st, self.sbuf2.data_ptr(), self.rbuf2.data_ptr(), ev[1].cuda_event,
+                ev[2].cuda_event, self._sp()), "ring step")
+            self._handle = None
+            return
         h = self.halo
         ymode = self._ymode()
         out_p = self.pack_x(self.prv, 1, ymode)
@@ -459,6 +514,7 @@ class RankWorker:
         self._handle = self._start_exchange(step_no, out_p, out_m)
         ev[1].record(self.stream)
         self._fused(g.Hx + h, g.Hx + g.Lx - h, flags, st)   # bulk columns
+        ev[2].record(self.stream)
 
     def step_end(self, step_no):
         g = self.geom
@@ -480,12 +536,15 @@ class RankWorker:
                         "collide")
         else:
             if self._handle is not None:
-                self._finish_exchange(self.prv, self._handle)
-                ev[2].record(self.stream)
+                # halo arrival -> unpack -> 3+3 border columns on the
+                # high-priority side stream, concurrent with the bulk kernel
+                cs = self.comm_stream
+                self._finish_exchange(self.prv, self._handle, cs)
                 h = self.halo
-                self._fused(g.Hx, g.Hx + h, self._flags, st)
-                self._fused(g.Hx + g.Lx - h, g.Hx + g.Lx, self._flags, st)
-            else:
+                self._fused(g.Hx, g.Hx + h, self._flags, st, cs)
+                self._fused(g.Hx + g.Lx - h, g.Hx + g.Lx, self._flags, st, cs)
+                self.stream.wait_stream(cs)
+            elif self._ring is None:
                 ev[2].record(self.stream)
         ev[3].record(self.stream)
         self._records.append(_StepRecord(step_no, slot, ev))

@@ -1,0 +1,58 @@
+"""torchrun worker for the multi-GPU tests (one process per GPU, NCCL).
+
+    python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 \
+        --master-port P tests/dist_run.py
+
+Runs sim.run with Np = world size (1-D X tiling, X faces exchanged over
+NCCL) for both schedules and compares the gathered state with the C oracle
+(bitwise, exact arithmetic) on rank 0.  Prints "DIST OK" on success.
+"""
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import paper_1703_00185_b200 as tl  # noqa: E402
+
+
+def main():
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    local = int(os.environ["LOCAL_RANK"])
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    dist.init_process_group("nccl", device_id=dev)
+    vs = tl.build_velocity_set("D2Q37")
+    p = tl.PhysicsParams(tau=0.8, gx=2e-6, gy=-1e-5, Twall_top=0.9 * vs.cs2,
+                         Twall_bot=1.1 * vs.cs2)
+    Lx, Ly, steps = 48 * world, 40, 9
+    want = None
+    if rank == 0:
+        from oracle import oracle as O
+        O.set_stencil(vs.c, vs.w, vs.cs2)
+        f0 = O.equilibrium(*O.rayleigh_taylor_macro(Lx, Ly, vs.cs2))
+        want, neg = O.run(f0, steps, O.params6(p.tau, p.gx, p.gy, p.dt, p.Twall_top,
+                                                 p.Twall_bot))
+    ok = True
+    for schedule in ("overlapped", "staged"):
+        res = tl.run(tl.SimConfig(Lx=Lx, Ly=Ly, Np=world, steps=steps, params=p,
+                                  init="rayleigh-taylor", schedule=schedule))
+        if rank == 0:
+            same = np.array_equal(res.populations, want)
+            print(f"schedule={schedule} world={world} bitwise={same} "
+                  f"mlups={res.mlups:.1f}", flush=True)
+            ok &= same
+        assert len(res.metrics) == steps
+    dist.barrier()
+    if rank == 0:
+        print("DIST OK" if ok else "DIST FAIL", flush=True)
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -76,6 +76,7 @@ def _worker(rank, world, port, Lx_tile, Ly, q):
         out_m = torch.from_numpy(pack_x(pops, c, -1, Lx_tile))
         w = _W(t, out_p.numel())
         fab = DistFabric()
+        assert not fab.native and fab.rank == rank and fab.Np == world
         for step in range(3):                   # repeated steps reuse the buffers
             h = fab.start_x(w, step, out_p, out_m)
             fab.finish_x(w, h, w.rbuf_plus, w.rbuf_minus)

@@ -1,0 +1,52 @@
+"""Multi-GPU paths (need >= 2 GPUs): one process per GPU over NCCL
+(torchrun) and in-process ranks on several GPUs (peer copies)."""
+
+import os
+import socket
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
+    pytest.skip("needs >= 2 CUDA devices", allow_module_level=True)
+
+import paper_1703_00185_b200 as tl  # noqa: E402
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.parametrize("n", [2, 4])
+def test_torchrun_nccl_ring_bitwise(n):
+    if torch.cuda.device_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={n}", "--master-addr", "127.0.0.1",
+           "--master-port", str(_port()), os.path.join(ROOT, "tests", "dist_run.py")]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    print(out.stdout[-3000:], out.stderr[-3000:])
+    assert out.returncode == 0
+    assert "DIST OK" in out.stdout
+
+
+def test_inprocess_ranks_on_two_gpus(orc):
+    vs = tl.build_velocity_set("D2Q37")
+    orc.set_stencil(vs.c, vs.w, vs.cs2)
+    p = tl.PhysicsParams(tau=0.8, gy=-1e-5, Twall_top=0.9 * vs.cs2, Twall_bot=1.1 * vs.cs2)
+    res = tl.run(tl.SimConfig(Lx=64, Ly=32, Np=4, steps=6, params=p,
+                              init="rayleigh-taylor", devices=(0, 1)))
+    f0 = orc.equilibrium(*orc.rayleigh_taylor_macro(64, 32, vs.cs2))
+    want, _ = orc.run(f0, 6, orc.params6(0.8, 0.0, -1e-5, 1.0, p.Twall_top, p.Twall_bot))
+    assert np.array_equal(res.populations, want)
