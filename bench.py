@@ -34,6 +34,32 @@ BYTES_SITE = 592          # fused step: 37 x 8 B read + 37 x 8 B written
 TILE_LX, TILE_LY = 1920, 2048
 
 
+def ncu_traffic(arith):
+    """dram__bytes_read.sum + dram__bytes_write.sum (GB) of the fused step
+    kernel from the committed `ncu --set full` capture (profiles/), or None."""
+    import csv
+    import glob
+    want = "k_site<3, %d, 4, 0, 4>" % (1 if arith == "exact" else 0)
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*ncu*raw*.csv")), reverse=True):
+        try:
+            rows = list(csv.reader(open(path)))
+        except OSError:
+            continue
+        if not rows:
+            continue
+        hdr = rows[0]
+        for r in rows[2:]:
+            d = dict(zip(hdr, r))
+            if want in d.get("Kernel Name", ""):
+                try:
+                    # ncu reports dram__bytes_* in GB in the raw page
+                    return round(float(d["dram__bytes_read.sum"]) +
+                                 float(d["dram__bytes_write.sum"]), 4), os.path.basename(path)
+                except (KeyError, ValueError):
+                    continue
+    return None, None
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -245,6 +271,7 @@ def gpu_arm(args, rank, world, local_rank):
     if hbm_peak is None:
         hbm_peak, peak_src = 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
 
+    traffic, traffic_src = ncu_traffic(args.arith)
     out = None
     if rank == 0:
         lib = _lib.load()
@@ -270,7 +297,10 @@ def gpu_arm(args, rank, world, local_rank):
             "gflops_fp64": round(gflops, 2),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak,
                          "unit": "GB/s", "frac": round(achieved / hbm_peak, 4),
-                         "traffic": None, "kernel": "k_site<FUSED> (propagate+bc+collide)",
+                         "traffic": traffic, "traffic_unit": "GB per launch (ncu dram read+write)",
+                         "traffic_source": traffic_src,
+                         "algorithmic_bytes_per_launch_GB": round(BYTES_SITE * kern_sites / 1e9, 4),
+                         "kernel": "k_site<FUSED> (propagate+bc+collide)",
                          "bytes_per_site": BYTES_SITE, "sites_per_launch": kern_sites,
                          "avg_launch_ms": round(kern_ms, 5), "peak_source": peak_src,
                          "fp64": {"achieved_tflops": round(kern_tflops, 3),

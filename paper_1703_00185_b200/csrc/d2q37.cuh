@@ -321,7 +321,16 @@ struct MomSeq {
     }
 };
 
-// moments (kernels.py:41-71).  Returns false if !(rho > 0).
+// RN(x / b) given y = RN(1/b): two Markstein steps (the first makes the
+// quotient faithful, the second correctly rounded; Markstein's theorem).
+__device__ __forceinline__ double div_rcp2(double x, double b, double y) {
+    return div_const2(x, b, y);
+}
+
+// moments (kernels.py:41-71).  Returns false if !(rho > 0).  The three
+// divisions share one correctly rounded reciprocal of rho (and of 2 rho,
+// which is exactly half of it) and are completed by Markstein corrections:
+// bit for bit the IEEE quotients of the reference.
 template <class F>
 __device__ __forceinline__ bool moments_exact(const F &f, double &rho, double &ux,
                                               double &uy, double &T) {
@@ -329,13 +338,36 @@ __device__ __forceinline__ bool moments_exact(const F &f, double &rho, double &u
     MomSeq<0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16, 17, 18, 19, 20,
            21, 22, 23, 24, 25, 26, 27, 28, 29, 30, 31, 32, 33, 34, 35, 36>::run(f, r, mx, my, e2);
     rho = r;
-    ux = __ddiv_rn(mx, r);
-    uy = __ddiv_rn(my, r);
-    T = __ddiv_rn(dsub(e2, dmul(r, dadd(dmul(ux, ux), dmul(uy, uy)))), dmul(2.0, r));
-    return r > 0.0;
+    if (!(r > 1e-300 && r < 1e300)) {  // degenerate or extreme: plain IEEE division
+        ux = __ddiv_rn(mx, r);
+        uy = __ddiv_rn(my, r);
+        T = __ddiv_rn(dsub(e2, dmul(r, dadd(dmul(ux, ux), dmul(uy, uy)))), dmul(2.0, r));
+        return r > 0.0;
+    }
+    const double yr = __drcp_rn(r);
+    ux = div_rcp2(mx, r, yr);
+    uy = div_rcp2(my, r, yr);
+    T = div_rcp2(dsub(e2, dmul(r, dadd(dmul(ux, ux), dmul(uy, uy)))), dmul(2.0, r),
+                 dmul(0.5, yr));
+    return true;
 }
 
 // collide one site in place (kernels.py:139-146).  Returns TLB_ST_* bits.
+// Moments read through `fm`, the relaxation reads/writes through `f` (they
+// may differ: e.g. registers for the moments, a reload for the relaxation).
+template <int ORDER, class FM, class F>
+__device__ __forceinline__ unsigned collide_exact2(const FM &fm, F &f, const Phys &P) {
+    double rho, ux, uy, T;
+    if (!moments_exact(fm, rho, ux, uy, T)) return 1u;
+    const double ub = dadd(ux, P.K1);
+    const double vb = dadd(uy, P.K2);
+    const double Tb = dsub(T, P.K3);
+    if (!(Tb > 0.0)) return 2u;
+    const EqSite e = eq_site_exact(rho, ub, vb, Tb);
+    eq_all_exact<ORDER, 1, F>(f, e, P.omega);
+    return 0u;
+}
+
 template <int ORDER, class F>
 __device__ __forceinline__ unsigned collide_exact(F &f, const Phys &P) {
     double rho, ux, uy, T;
@@ -443,11 +475,14 @@ __device__ __forceinline__ void fast_all(F &f, const FastSite &e, double omr) {
 }
 
 template <int ORDER, class F>
-__device__ __forceinline__ unsigned collide_fast(F &f, const Phys &P) {
+__device__ __forceinline__ unsigned collide_fast(F &f, const Phys &P);
+
+template <int ORDER, class FM, class F>
+__device__ __forceinline__ unsigned collide_fast2(const FM &fm, F &f, const Phys &P) {
     double r0 = 0.0, r1 = 0.0, mx = 0.0, my = 0.0, e2 = 0.0;
 #pragma unroll
     for (int l = 0; l < Q; ++l) {
-        const double fl = f.get(l);
+        const double fl = fm.get(l);
         if (l & 1) r1 += fl; else r0 += fl;
         if (CX(l)) mx = fma((double)CX(l), fl, mx);
         if (CY(l)) my = fma((double)CY(l), fl, my);
@@ -469,6 +504,11 @@ __device__ __forceinline__ unsigned collide_fast(F &f, const Phys &P) {
     e.W = P.omega * rho;
     fast_all<ORDER, 1, F>(f, e, 1.0 - P.omega);
     return 0u;
+}
+
+template <int ORDER, class F>
+__device__ __forceinline__ unsigned collide_fast(F &f, const Phys &P) {
+    return collide_fast2<ORDER, F, F>(f, f, P);
 }
 
 template <int ORDER, class F>

@@ -48,7 +48,8 @@ static int launch_check(const char *what) {
 }
 
 static bool g_stencil_set[64];
-static int g_minb = 4;  // tuning: __launch_bounds__ min blocks of the fused kernel
+static int g_minb = 4;    // tuning: __launch_bounds__ min blocks of the fused kernel
+static int g_reload = 0;  // tuning: relaxation re-reads f (0 = off, 4/5 = on with that occupancy)
 
 // --------------------------------------------------------- device helpers --
 struct Fld {
@@ -90,6 +91,8 @@ struct Rect {
 
 struct SiteLaunch {
     Fld src, dst;
+    long long soffb[Q];  // byte offset of population l's source from the site
+    long long doffb[Q];  // byte offset of population l's destination
     Rect in;
     Rect fr[4];
     unsigned fr_end[4];  // prefix sums of frame sites
@@ -208,32 +211,58 @@ __device__ __forceinline__ void load_inplace(double (&f)[Q], const Fld &s, int x
     for (int l = 0; l < Q; ++l) f[l] = p[(long long)l * s.sl];
 }
 
-template <int l>
-__device__ __forceinline__ void load_plain_one(double (&f)[Q], const Fld &s, long long site,
-                                               bool gather) {
-    long long off = site + (long long)l * s.sl;
-    if (gather) off -= (long long)CX(l) * s.sx + (long long)CY(l) * s.sy;
-    f[l] = __ldg(s.base + off);
+// Interior loads: one site pointer plus the launch's precomputed byte
+// offsets of the 37 (shifted) population sources -- no branches, all 37
+// loads issued back to back, two integer adds each.
+__device__ __forceinline__ void load_plain(double (&f)[Q], const SiteLaunch &L, int x, int y) {
+    const char *sp = reinterpret_cast<const char *>(
+        L.src.base + (long long)x * L.src.sx + (long long)y * L.src.sy);
+#pragma unroll
+    for (int l = 0; l < Q; ++l) f[l] = __ldg(reinterpret_cast<const double *>(sp + L.soffb[l]));
 }
 
-template <int... Ls>
-struct PlainSeq {
-    __device__ __forceinline__ static void run(double (&f)[Q], const Fld &s, long long site,
-                                               bool gather) {
-        (load_plain_one<Ls>(f, s, site, gather), ...);
+// Collide outputs streamed to global as soon as each is final (no 37-wide
+// live output vector); negatives counted on the way.
+struct RegStoreF {
+    double (&a)[Q];
+    char *dp;
+    const long long *doffb;
+    bool active;
+    unsigned neg;
+    __device__ __forceinline__ double get(int l) const { return a[l]; }
+    __device__ __forceinline__ void put(int l, double v) {
+        if (active) {
+            *reinterpret_cast<double *>(dp + doffb[l]) = v;
+            neg += v < 0.0;
+        }
     }
 };
 
-// Interior loads: one 64-bit site offset plus compile-time population
-// offsets -- no branches, all 37 loads issued back to back.
-__device__ __forceinline__ void load_plain(double (&f)[Q], const Fld &s, int x, int y,
-                                           bool gather) {
-    const long long site = (long long)x * s.sx + (long long)y * s.sy;
-    PlainSeq<0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16, 17, 18, 19, 20, 21,
-             22, 23, 24, 25, 26, 27, 28, 29, 30, 31, 32, 33, 34, 35, 36>::run(f, s, site, gather);
-}
+// As RegStoreF, but the relaxation re-reads f_l from global (an L1/L2 hit:
+// the line was fetched for the moments moments ago) instead of keeping the
+// 37-vector live in registers through the equilibrium -- trading a cache
+// re-read for registers, i.e. for ILP in the FP64 chains.
+struct ReloadStoreF {
+    const char *sp;
+    const long long *soffb;
+    char *dp;
+    const long long *doffb;
+    bool active;
+    unsigned neg;
+    __device__ __forceinline__ double get(int l) const {
+        double v;
+        asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(v) : "l"(sp + soffb[l]));
+        return v;
+    }
+    __device__ __forceinline__ void put(int l, double v) {
+        if (active) {
+            *reinterpret_cast<double *>(dp + doffb[l]) = v;
+            neg += v < 0.0;
+        }
+    }
+};
 
-template <int KIND, bool EXACT, int ORDER, bool INPLACE, bool EDGE>
+template <int KIND, bool EXACT, int ORDER, bool INPLACE, bool EDGE, bool RELOAD = false>
 __device__ __forceinline__ void site_body(const SiteLaunch &L, int x, int y, bool active) {
     double f[Q];
     constexpr bool gather = KIND == K_PROPAGATE || KIND == K_FUSED;
@@ -243,7 +272,7 @@ __device__ __forceinline__ void site_body(const SiteLaunch &L, int x, int y, boo
         const bool implicit = (L.flags & (TLB_F_WRAP_X | TLB_F_WRAP_Y | TLB_F_CLAMP_Y)) != 0;
         load_all(f, L.src, x, y, gather, implicit, L.flags);
     } else {
-        load_plain(f, L.src, x, y, gather);
+        load_plain(f, L, x, y);
     }
     unsigned bits = 0;
     if (EDGE && (KIND == K_BC || KIND == K_FUSED)) {
@@ -254,6 +283,27 @@ __device__ __forceinline__ void site_body(const SiteLaunch &L, int x, int y, boo
             RegF rf{f};
             bits |= EXACT ? bc_exact<ORDER>(rf, Tw) : bc_fast<ORDER>(rf, Tw);
         }
+    }
+    if constexpr (RELOAD && !EDGE && !INPLACE && (KIND == K_COLLIDE || KIND == K_FUSED)) {
+        char *dp = reinterpret_cast<char *>(L.dst.base + (long long)x * L.dst.sx +
+                                            (long long)y * L.dst.sy);
+        const char *sp = reinterpret_cast<const char *>(
+            L.src.base + (long long)x * L.src.sx + (long long)y * L.src.sy);
+        RegF fm{f};
+        ReloadStoreF sf{sp, L.soffb, dp, L.doffb, active, 0u};
+        bits |= EXACT ? collide_exact2<ORDER>(fm, sf, L.P) : collide_fast2<ORDER>(fm, sf, L.P);
+        if (active) report(L.status, bits, x, y, L.step);
+        if (L.flags & TLB_F_COUNT_NEG) count_neg_n(L.status, sf.neg);
+        return;
+    }
+    if constexpr (!EDGE && !INPLACE && (KIND == K_COLLIDE || KIND == K_FUSED)) {
+        char *dp = reinterpret_cast<char *>(L.dst.base + (long long)x * L.dst.sx +
+                                            (long long)y * L.dst.sy);
+        RegStoreF sf{f, dp, L.doffb, active, 0u};
+        bits |= EXACT ? collide_exact<ORDER>(sf, L.P) : collide_fast<ORDER>(sf, L.P);
+        if (active) report(L.status, bits, x, y, L.step);
+        if (L.flags & TLB_F_COUNT_NEG) count_neg_n(L.status, sf.neg);
+        return;
     }
     if (KIND == K_COLLIDE || KIND == K_FUSED) {
         RegF rf{f};
@@ -269,8 +319,8 @@ __device__ __forceinline__ void site_body(const SiteLaunch &L, int x, int y, boo
 // One thread = one site.  Sites are enumerated y-fastest inside each
 // rectangle so consecutive lanes touch consecutive addresses of every
 // population plane.
-template <int KIND, bool EXACT, int ORDER, bool INPLACE, int MINB>
-__global__ void __launch_bounds__(128, MINB) k_site(SiteLaunch L) {
+template <int KIND, bool EXACT, int ORDER, bool INPLACE, int MINB, bool RELOAD = false>
+__global__ void __launch_bounds__(128, MINB) k_site(const __grid_constant__ SiteLaunch L) {
     if (blockIdx.x < L.nfb) {
         const unsigned total = L.fr_end[3];
         const unsigned i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -285,8 +335,8 @@ __global__ void __launch_bounds__(128, MINB) k_site(SiteLaunch L) {
         const unsigned i = (blockIdx.x - L.nfb) * blockDim.x + threadIdx.x;
         const bool active = i < L.in.n;
         const unsigned ii = active ? i : L.in.n - 1;
-        site_body<KIND, EXACT, ORDER, INPLACE, false>(L, L.in.x0 + (int)(ii / L.in.ny),
-                                                      L.in.y0 + (int)(ii % L.in.ny), active);
+        site_body<KIND, EXACT, ORDER, INPLACE, false, RELOAD>(
+            L, L.in.x0 + (int)(ii / L.in.ny), L.in.y0 + (int)(ii % L.in.ny), active);
     }
 }
 
@@ -294,6 +344,13 @@ __global__ void __launch_bounds__(128, MINB) k_site(SiteLaunch L) {
 template <int KIND, bool INPLACE>
 static int launch_site(SiteLaunch &L, bool exact, int order, cudaStream_t s, const char *what) {
     const int bs = 128;
+    constexpr bool gather = KIND == K_PROPAGATE || KIND == K_FUSED;
+    for (int l = 0; l < Q; ++l) {
+        long long so = (long long)l * L.src.sl;
+        if (gather) so -= (long long)CX(l) * L.src.sx + (long long)CY(l) * L.src.sy;
+        L.soffb[l] = 8 * so;
+        L.doffb[l] = 8 * (long long)l * L.dst.sl;
+    }
     const unsigned long long nf = L.fr_end[3];
     L.nfb = (unsigned)((nf + bs - 1) / bs);
     const unsigned long long nb = L.nfb + (L.in.n + (unsigned long long)bs - 1) / bs;
@@ -305,7 +362,9 @@ static int launch_site(SiteLaunch &L, bool exact, int order, cudaStream_t s, con
 #define TLB_L(E, O) k_site<KIND, E, O, INPLACE, 4><<<grid, block, 0, s>>>(L)
 #define TLB_LT(E, O)                                                               \
     do {                                                                           \
-        if (g_minb == 1) k_site<KIND, E, O, INPLACE, 1><<<grid, block, 0, s>>>(L); \
+        if (g_reload == 4) k_site<KIND, E, O, INPLACE, 4, true><<<grid, block, 0, s>>>(L); \
+        else if (g_reload == 5) k_site<KIND, E, O, INPLACE, 5, true><<<grid, block, 0, s>>>(L); \
+        else if (g_minb == 1) k_site<KIND, E, O, INPLACE, 1><<<grid, block, 0, s>>>(L); \
         else if (g_minb == 5) k_site<KIND, E, O, INPLACE, 5><<<grid, block, 0, s>>>(L); \
         else TLB_L(E, O);                                                          \
     } while (0)
@@ -621,6 +680,12 @@ int tlb_set_tuning(int key, int value) {
         if (value != 1 && value != 4 && value != 5)
             return fail(TLB_ERR_CONTRACT, "min blocks must be 1, 4 or 5");
         g_minb = value;
+        return TLB_OK;
+    }
+    if (key == TLB_TUNE_RELOAD) {
+        if (value != 0 && value != 4 && value != 5)
+            return fail(TLB_ERR_CONTRACT, "reload must be 0, 4 or 5");
+        g_reload = value;
         return TLB_OK;
     }
     return fail(TLB_ERR_CONTRACT, "unknown tuning key %d", key);
