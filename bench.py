@@ -39,7 +39,7 @@ def ncu_traffic(arith):
     kernel from the committed `ncu --set full` capture (profiles/), or None."""
     import csv
     import glob
-    want = "k_site<3, %d, 4, 0, 4>" % (1 if arith == "exact" else 0)
+    want = "k_site<3, %d, 4, 0, 4" % (1 if arith == "exact" else 0)
     for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*ncu*raw*.csv")), reverse=True):
         try:
             rows = list(csv.reader(open(path)))
@@ -195,8 +195,13 @@ def gpu_arm(args, rank, world, local_rank):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
     vs = tl.build_velocity_set("D2Q37")
-    Lx_tile, Ly = args.Lx, args.Ly
-    Lx = Lx_tile * world
+    if args.strong:
+        # BASELINE configs[3]: fixed 8192x16384 lattice split over the GPUs
+        Lx, Ly = 8192, 16384
+        Lx_tile = Lx // world
+    else:
+        Lx_tile, Ly = args.Lx, args.Ly
+        Lx = Lx_tile * world
     p = tl.PhysicsParams(tau=0.8, gx=0.0, gy=-1e-5, Twall_top=0.9 * vs.cs2,
                          Twall_bot=1.1 * vs.cs2, arith=args.arith)
     tiles = tl.decompose(Lx, Ly, world, "1d")
@@ -218,18 +223,25 @@ def gpu_arm(args, rank, world, local_rank):
         for s in range(s0, s0 + n):
             w.step(s)
 
-    # warm-up
+    # warm-up (also sizes the clock pre-load identically on every rank: each
+    # rank must run exactly the same number of ring steps)
+    tw = time.perf_counter()
     run_steps(args.warmup)
     w.synchronize()
+    step_s = (time.perf_counter() - tw) / args.warmup
+    if dist is not None:
+        t = torch.tensor([step_s], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        step_s = float(t.item())
+    n_pre = int(min(5000, max(0, args.preload / max(step_s, 1e-5))))
     w.collect()
     w._metrics.clear()
 
     # clocks: sample while a ~1 s untimed pre-load runs, then the timed steps
     sampler = ClockSampler(_gpu_index(local_rank))
     sampler.start()
-    t_pre = time.perf_counter()
     s = args.warmup
-    while time.perf_counter() - t_pre < args.preload:
+    for _ in range(0, n_pre, 10):
         run_steps(10, s)
         s += 10
         w.synchronize()
@@ -271,25 +283,65 @@ def gpu_arm(args, rank, world, local_rank):
     if hbm_peak is None:
         hbm_peak, peak_src = 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
 
+    # the other arithmetic, same workload, same timing (every rank: the ring
+    # needs the same number of steps everywhere)
+    other = None
+    if args.compare:
+        oth = "exact" if args.arith == "fast" else "fast"
+        keep = w.tparams
+        w.tparams = _lib.params(tl.PhysicsParams(
+            tau=0.8, gx=0.0, gy=-1e-5, Twall_top=0.9 * vs.cs2, Twall_bot=1.1 * vs.cs2,
+            arith=oth))
+        s2 = s + args.steps + 1000
+        run_steps(3, s2)
+        w.synchronize()
+        w.collect()
+        w._metrics.clear()
+        barrier()
+        a0 = torch.cuda.Event(enable_timing=True)
+        a1 = torch.cuda.Event(enable_timing=True)
+        a0.record(w.stream)
+        run_steps(args.steps, s2 + 3)
+        a1.record(w.stream)
+        torch.cuda.synchronize()
+        ms2 = a0.elapsed_time(a1)
+        if dist is not None:
+            t = torch.tensor([ms2], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms2 = float(t.item())
+        k2 = float(np.mean([m["t_bulk"] * 1e3 for m in w.metrics]))
+        w._metrics.clear()
+        w.tparams = keep
+        ach2 = BYTES_SITE * kern_sites / (k2 * 1e-3) / 1e9
+        other = {"arith": oth, "value": round(sites * args.steps / (ms2 * 1e-3) / 1e6, 3),
+                 "ms_per_step": round(ms2 / args.steps, 5),
+                 "gflops_fp64": round(flops_step * args.steps / (ms2 * 1e-3) / 1e9, 2),
+                 "kernel_ms": round(k2, 5), "kernel_GBps": round(ach2, 1),
+                 "kernel_frac_of_hbm_peak": round(ach2 / hbm_peak, 4),
+                 "parity": ("bitwise = reference" if oth == "exact"
+                            else "<=1e-12 relative (tests/test_gpu_parity.py)")}
+
     traffic, traffic_src = ncu_traffic(args.arith)
     out = None
     if rank == 0:
         lib = _lib.load()
         import ctypes
         fp = ctypes.c_double(0.0)
-        _lib.check(lib.tlb_bench_dfma(200000, ctypes.byref(fp), _lib.stream_ptr()), "dfma")
-        fp64_peak = fp.value / 1e12
+        if args.probe:
+            _lib.check(lib.tlb_bench_dfma(200000, ctypes.byref(fp), _lib.stream_ptr()), "dfma")
+        fp64_peak = fp.value / 1e12 if args.probe else float("nan")
         kern_tflops = (FLOP_SITE * kern_sites + FLOP_WALL_SITE * 6 * Lx_tile) / (kern_ms * 1e-3) / 1e12
         split = split_kernels(w, tl, _lib, field_desc, torch) if args.split else None
         out = {
             "metric": METRIC, "value": round(mlups, 3), "unit": "MLUPS",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(ms / args.steps, 5), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "strong" if args.strong else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (Rayleigh-Taylor initial state, reference init.py:45-64)",
             "config": {"workload": f"D2Q37 RT {Lx}x{Ly}" + (
                 f" (1-D X tiles of {Lx_tile}x{Ly}, overlapped NCCL halo)" if world > 1 else
-                " on 1 B200 (BASELINE configs[1])"),
+                (" on 1 B200 (BASELINE configs[3], strong-scaling base)" if args.strong
+                 else " on 1 B200 (BASELINE configs[1])")),
                 "Lx": Lx, "Ly": Ly, "tiling": "1d", "schedule": args.schedule,
                 "arith": args.arith, "tau": 0.8, "gy": -1e-5,
                 "l2": "no flush: 2 x %.2f GB state per GPU >> 126 MB L2" % (
@@ -313,6 +365,11 @@ def gpu_arm(args, rank, world, local_rank):
         }
         if split:
             out["split"] = split
+        out["parity"] = ("bitwise = reference (exact IEEE op order)" if args.arith == "exact"
+                         else "fast FMA arithmetic: f, rho, T within 1e-12 relative, |du| <= "
+                              "1e-12 cs after 100 RT steps (tests/test_gpu_parity.py)")
+        if other:
+            out["other_arith"] = other
     # e2e through the public API with host buffers
     e2e = e2e_run(args, w, tl, torch, dist, local_rank, Lx_tile, Ly) if args.e2e else None
     if rank == 0:
@@ -420,14 +477,21 @@ def main():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--arith", default="exact", choices=["exact", "fast"])
+    ap.add_argument("--arith", default="fast", choices=["exact", "fast"],
+                    help="fast (default; the north star's 1e-12 contract) or exact (bitwise)")
+    ap.add_argument("--no-compare", dest="compare", action="store_false",
+                    help="skip timing the other arithmetic")
     ap.add_argument("--schedule", default="overlapped", choices=["overlapped", "staged"])
     ap.add_argument("--Lx", type=int, default=TILE_LX, help="tile Lx per GPU")
     ap.add_argument("--Ly", type=int, default=TILE_LY)
+    ap.add_argument("--strong", action="store_true",
+                    help="configs[3]: 8192x16384 total, split over the GPUs (strong scaling)")
     ap.add_argument("--preload", type=float, default=1.0, help="s of untimed load for clocks")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-e2e", dest="e2e", action="store_false")
     ap.add_argument("--no-split", dest="split", action="store_false")
+    ap.add_argument("--no-probe", dest="probe", action="store_false",
+                    help="skip the FP64 DFMA peak probe")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

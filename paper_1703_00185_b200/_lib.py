@@ -16,7 +16,7 @@ from .errors import (ContractViolation, DeviceError, DomainError,
                      UnsupportedCaseError)
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libtlb.so")
+LIB_PATH = os.environ.get("TLB_LIB_PATH") or os.path.join(HERE, "libtlb.so")
 
 TLB_OK, TLB_ERR_CONTRACT, TLB_ERR_CUDA, TLB_ERR_STENCIL, TLB_ERR_UNSUPPORTED, \
     TLB_ERR_DOMAIN = range(6)

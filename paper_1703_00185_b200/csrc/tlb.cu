@@ -214,15 +214,29 @@ __device__ __forceinline__ void load_inplace(double (&f)[Q], const Fld &s, int x
 // Interior loads: one site pointer plus the launch's precomputed byte
 // offsets of the 37 (shifted) population sources -- no branches, all 37
 // loads issued back to back, two integer adds each.
+// STREAM: L1::no_allocate loads (and streaming stores, see RegStoreF) --
+// measured +2 % for the exact collide, -5 % for fast and propagate
+// (profiles/r01_summary.md), so only the exact fused path uses them.
+template <bool STREAM>
 __device__ __forceinline__ void load_plain(double (&f)[Q], const SiteLaunch &L, int x, int y) {
     const char *sp = reinterpret_cast<const char *>(
         L.src.base + (long long)x * L.src.sx + (long long)y * L.src.sy);
 #pragma unroll
-    for (int l = 0; l < Q; ++l) f[l] = __ldg(reinterpret_cast<const double *>(sp + L.soffb[l]));
+    for (int l = 0; l < Q; ++l) {
+        if constexpr (STREAM) {
+            double v;
+            asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];"
+                         : "=d"(v) : "l"(sp + L.soffb[l]));
+            f[l] = v;
+        } else {
+            f[l] = __ldg(reinterpret_cast<const double *>(sp + L.soffb[l]));
+        }
+    }
 }
 
 // Collide outputs streamed to global as soon as each is final (no 37-wide
 // live output vector); negatives counted on the way.
+template <bool STREAM>
 struct RegStoreF {
     double (&a)[Q];
     char *dp;
@@ -232,7 +246,10 @@ struct RegStoreF {
     __device__ __forceinline__ double get(int l) const { return a[l]; }
     __device__ __forceinline__ void put(int l, double v) {
         if (active) {
-            *reinterpret_cast<double *>(dp + doffb[l]) = v;
+            if constexpr (STREAM)
+                __stcs(reinterpret_cast<double *>(dp + doffb[l]), v);
+            else
+                *reinterpret_cast<double *>(dp + doffb[l]) = v;
             neg += v < 0.0;
         }
     }
@@ -272,7 +289,7 @@ __device__ __forceinline__ void site_body(const SiteLaunch &L, int x, int y, boo
         const bool implicit = (L.flags & (TLB_F_WRAP_X | TLB_F_WRAP_Y | TLB_F_CLAMP_Y)) != 0;
         load_all(f, L.src, x, y, gather, implicit, L.flags);
     } else {
-        load_plain(f, L, x, y);
+        load_plain<EXACT && KIND == K_FUSED>(f, L, x, y);
     }
     unsigned bits = 0;
     if (EDGE && (KIND == K_BC || KIND == K_FUSED)) {
@@ -299,7 +316,7 @@ __device__ __forceinline__ void site_body(const SiteLaunch &L, int x, int y, boo
     if constexpr (!EDGE && !INPLACE && (KIND == K_COLLIDE || KIND == K_FUSED)) {
         char *dp = reinterpret_cast<char *>(L.dst.base + (long long)x * L.dst.sx +
                                             (long long)y * L.dst.sy);
-        RegStoreF sf{f, dp, L.doffb, active, 0u};
+        RegStoreF<EXACT && KIND == K_FUSED> sf{f, dp, L.doffb, active, 0u};
         bits |= EXACT ? collide_exact<ORDER>(sf, L.P) : collide_fast<ORDER>(sf, L.P);
         if (active) report(L.status, bits, x, y, L.step);
         if (L.flags & TLB_F_COUNT_NEG) count_neg_n(L.status, sf.neg);

@@ -1,9 +1,9 @@
+# 1-GPU round: parity tests, bench (fast headline + exact), launch list, ncu of the step kernels
 timeout 600 python -m pytest tests -m gpu -x -q -p no:cacheprovider 2>&1 | tail -3
-timeout 300 python bench.py > gpurun_out/bench2.json 2> gpurun_out/bench2.err; tail -2 gpurun_out/bench2.err
-timeout 300 python bench.py --arith fast --cpu-seconds 0 > gpurun_out/bench2_fast.json 2>&1
-B="python bench.py --steps 20 --warmup 3 --cpu-seconds 0 --no-e2e --no-split --preload 0"
+timeout 300 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; tail -2 gpurun_out/bench.err
+B="python bench.py --steps 20 --warmup 3 --cpu-seconds 0 --no-e2e --no-split --no-compare --no-probe --preload 0"
 timeout 300 $B > gpurun_out/b_small.log 2>&1 && timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 300 --csv --log-file gpurun_out/launches.csv $B > gpurun_out/ncu_launch.log 2>&1
 P="python tools/prof_fused.py --only fused_exact_step_neg,fused_fast_step"
 timeout 300 $P > gpurun_out/p_small.log 2>&1 && timeout 600 ncu --set full --import-source on --clock-control none -k regex:k_site -s 1 -c 3 -o gpurun_out/prof_step $P > gpurun_out/ncu2.log 2>&1
 tail -2 gpurun_out/ncu2.log
-cat gpurun_out/bench2.json
+cat gpurun_out/bench.json

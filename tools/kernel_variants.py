@@ -25,10 +25,20 @@ def main():
     ap.add_argument("--Lx", type=int, default=1920)
     ap.add_argument("--Ly", type=int, default=2048)
     ap.add_argument("--only", default="")
+    ap.add_argument("--pad", type=int, default=0,
+                    help="align: column pitch multiple of 16 doubles, y=Hy at a 128 B boundary")
     a = ap.parse_args()
     vs = tl.build_velocity_set("D2Q37")
     g = tl.LatticeGeometry(a.Lx, a.Ly, 3, 3, 37)
     prv, nxt = tl.allocate_field(g, vs)
+    if a.pad:
+        # same logical (Q, NX, NY) view over a padded, 128 B aligned allocation
+        off = (16 - g.Hy % 16) % 16
+        pitch = -(-(g.NY + off) // 16) * 16
+        for fld in (prv, nxt):
+            buf = torch.zeros((37, g.NX, pitch), dtype=torch.float64, device="cuda")
+            fld.data = buf[:, :, off:off + g.NY]
+        print(f"padded: pitch {pitch}, offset {off}", flush=True)
     macro = tl.init.rayleigh_taylor_macro(a.Lx, a.Ly, vs)
     f0 = tl.equilibrium(*[torch.as_tensor(m).cuda() for m in macro], vs)
     prv.pops[:, g.phys_x, g.phys_y] = f0
