@@ -91,6 +91,11 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
+            # nvidia-smi can take seconds to start on a multi-GPU box: wait for
+            # its first sample so the load phase is actually observed
+            t0 = time.time()
+            while not self.rows and time.time() - t0 < 15 and self.proc.poll() is None:
+                time.sleep(0.05)
         except OSError:
             self.proc = None
 
