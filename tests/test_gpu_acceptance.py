@@ -255,7 +255,7 @@ def test_aos_layout_same_bits(vs):
 def test_device_output_and_explicit_f0(vs):
     p = tl.PhysicsParams(tau=0.8, gy=-1e-5, Twall_top=0.9 * vs.cs2, Twall_bot=1.1 * vs.cs2)
     host = tl.run(tl.SimConfig(Lx=32, Ly=16, steps=3, params=p, init="rayleigh-taylor"))
-    f0 = tl.build_initial_state("rayleigh-taylor", 32, 16, vs)
+    f0 = tl.init.build_initial_state("rayleigh-taylor", 32, 16, vs)
     dev = tl.run(tl.SimConfig(Lx=32, Ly=16, steps=3, params=p, output="device"), f0=f0)
     assert dev.populations.is_cuda
     assert np.array_equal(dev.populations.cpu().numpy(), host.populations)
