@@ -212,6 +212,13 @@ int tlb_ring_step(tlb_ring_t ring, const TlbField *prv, const TlbField *nxt,
                   double *sbuf, double *rbuf, void *ev_bulk0, void *ev_bulk1,
                   tlb_stream_t stream);
 
+/* Snapshot image (io.write_pgm, io.py:13-24): min-max normalised 8-bit
+ * quantisation of a (nx, ny) field with row stride ld into img (nx*ny bytes,
+ * PGM row order: top row = largest y).  minmax2 is 2 x u64 device scratch. */
+int tlb_pgm_image(const double *v, int64_t nx, int64_t ny, int64_t ld,
+                  unsigned long long *minmax2, unsigned char *img,
+                  tlb_stream_t stream);
+
 /* Tuning knobs (process-wide): TLB_TUNE_MINBLOCKS selects the
  * __launch_bounds__ minimum CTAs/SM of the fused kernel (1 = compiler's
  * choice, 4 = default, 5). */

@@ -92,6 +92,7 @@ SIGNATURES = [
     ("tlb_ring_destroy", _INT, [_P]),
     ("tlb_ring_exchange", _INT, [_P, _FP, _INT, _P, _P, _P]),
     ("tlb_ring_step", _INT, [_P, _FP, _FP, _PP, _INT, _P, _P, _P, _P, _P, _P]),
+    ("tlb_pgm_image", _INT, [_P, _I64, _I64, _I64, _P, _P, _P]),
     ("tlb_set_tuning", _INT, [_INT, _INT]),
     ("tlb_bench_dfma", _INT, [_I64, ctypes.POINTER(ctypes.c_double), _P]),
 ]

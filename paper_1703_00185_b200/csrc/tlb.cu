@@ -1020,3 +1020,69 @@ extern "C" int tlb_bench_dfma(int64_t iters, double *flops_per_s, tlb_stream_t s
 
 // 1-D X ring across GPUs (NCCL), same translation unit
 #include "tlb_ring.cuh"
+
+// ------------------------------------------------------ snapshot images --
+// io.write_pgm (io.py:13-24) on the device: min/max of a (nx, ny) field and
+// the 8-bit quantisation ((v - lo) / span * 255).round() with numpy's
+// round-half-even (rint), rows top to bottom (decreasing y).  Only the
+// nx*ny bytes of the image cross PCIe.
+__device__ __forceinline__ unsigned long long ord_key(double v) {
+    unsigned long long b = (unsigned long long)__double_as_longlong(v);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double ord_val(unsigned long long k) {
+    return __longlong_as_double((long long)((k >> 63) ? (k & 0x7fffffffffffffffull) : ~k));
+}
+
+__global__ void k_mm_init(unsigned long long *mm) {
+    mm[0] = ~0ull;
+    mm[1] = 0ull;
+}
+
+__global__ void k_minmax(const double *v, long long nx, long long ny, long long ld,
+                         unsigned long long *out) {
+    unsigned long long lo = ~0ull, hi = 0ull;
+    const long long n = nx * ny;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const unsigned long long k = ord_key(v[(i / ny) * ld + i % ny]);
+        lo = k < lo ? k : lo;
+        hi = k > hi ? k : hi;
+    }
+    for (int o = 16; o; o >>= 1) {
+        const unsigned long long a = __shfl_xor_sync(0xffffffffu, lo, o);
+        const unsigned long long b = __shfl_xor_sync(0xffffffffu, hi, o);
+        lo = a < lo ? a : lo;
+        hi = b > hi ? b : hi;
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(out, lo);
+        atomicMax(out + 1, hi);
+    }
+}
+
+__global__ void k_quantize(const double *v, long long nx, long long ny, long long ld,
+                           const unsigned long long *mm, unsigned char *img) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nx * ny) return;
+    const long long x = i / ny, y = i % ny;
+    const double lo = ord_val(mm[0]), hi = ord_val(mm[1]);
+    const double span = hi > lo ? hi - lo : 1.0;
+    const double q = rint(__dmul_rn(__ddiv_rn(__dsub_rn(v[x * ld + y], lo), span), 255.0));
+    img[(ny - 1 - y) * nx + x] = (unsigned char)q;
+}
+
+extern "C" int tlb_pgm_image(const double *v, int64_t nx, int64_t ny, int64_t ld,
+                             unsigned long long *minmax2, unsigned char *img,
+                             tlb_stream_t stream) {
+    if (nx <= 0 || ny <= 0) return fail(TLB_ERR_CONTRACT, "empty field");
+    cudaStream_t s = (cudaStream_t)stream;
+    k_mm_init<<<1, 1, 0, s>>>(minmax2);
+    const long long n = nx * ny;
+    const unsigned nb = (unsigned)((n + 255) / 256 < 1184 ? (n + 255) / 256 : 1184);
+    k_minmax<<<nb, 256, 0, s>>>(v, nx, ny, ld, minmax2);
+    int e = launch_check("minmax");
+    if (e) return e;
+    k_quantize<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(v, nx, ny, ld, minmax2, img);
+    return launch_check("quantize");
+}

@@ -168,6 +168,20 @@ def main():
         ref_init.equilibrium = orig
     np.savez(os.path.join(HERE, "random_init.npz"), **captured)
 
+    # ------------------------------------------------------------- io --
+    import tempfile
+    import thermolb.io as ref_io
+    T = r["rt_f20_macro"][3]
+    with tempfile.TemporaryDirectory() as td:
+        ref_io.write_pgm(os.path.join(td, "t.pgm"), T)
+        pgm = open(os.path.join(td, "t.pgm"), "rb").read()
+        from thermolb.geometry import MacroFields
+        mf = MacroFields(*r["rt_f20_macro"][:, :4, :3])
+        ref_io.write_macro_csv(os.path.join(td, "m.csv"), mf)
+        csv_txt = open(os.path.join(td, "m.csv")).read()
+    np.savez(os.path.join(HERE, "io.npz"), T=T, pgm=np.frombuffer(pgm, dtype=np.uint8),
+             macro_small=r["rt_f20_macro"][:, :4, :3], csv=np.array(csv_txt))
+
     # ---------------------------------------------------- fingerprints --
     fp = {"w": sha16(vs.w), "cs2": float.hex(float(vs.cs2))}
     cfg = SimConfig(Lx=256, Ly=128, model="D2Q37", Np=1, tiling="1d",

@@ -264,3 +264,15 @@ def test_device_output_and_explicit_f0(vs):
 def test_two_d_tiling_rejected(vs):
     with pytest.raises(tl.UnsupportedCaseError):
         tl.run(tl.SimConfig(Lx=16, Ly=16, Np=4, tiling=(2, 2), steps=1))
+
+
+def test_pgm_bytes_match_reference(tmp_path):
+    """io.write_pgm (io.py:13-24) on the device: byte-identical image."""
+    from conftest import golden
+    from paper_1703_00185_b200 import io as tio
+    g = golden("io.npz")
+    tio.write_pgm(tmp_path / "t.pgm", g["T"])
+    assert (tmp_path / "t.pgm").read_bytes() == g["pgm"].tobytes()
+    # a device (strided) view gives the same bytes
+    t = torch.as_tensor(np.pad(g["T"], ((0, 0), (3, 3)))).cuda()[:, 3:-3]
+    assert tio.pgm_bytes(t) == g["pgm"].tobytes()

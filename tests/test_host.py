@@ -162,3 +162,25 @@ def test_product_does_not_import_oracle():
                 assert "oracle" not in txt.replace("oracle/", "").lower() or \
                     "import oracle" not in txt, f
                 assert "from oracle" not in txt and "import oracle" not in txt, f
+
+
+# -------------------------------------------------------------------- io --
+
+def test_macro_csv_matches_reference(tmp_path):
+    from paper_1703_00185_b200 import io as tio
+    g = golden("io.npz")
+    m = g["macro_small"]
+    tio.write_macro_csv(tmp_path / "m.csv", tl.MacroFields(*m))
+    assert (tmp_path / "m.csv").read_text() == str(g["csv"])
+
+
+def test_load_config(tmp_path):
+    from paper_1703_00185_b200 import io as tio
+    p = tmp_path / "c.yaml"
+    p.write_text("Lx: 8\nLy: 4\n")
+    assert tio.load_config(p) == {"Lx": 8, "Ly": 4}
+    p.write_text("- 1\n- 2\n")
+    with pytest.raises(tl.ConfigurationError):
+        tio.load_config(p)
+    with pytest.raises(tl.ConfigurationError):
+        tio.load_config(tmp_path / "missing.yaml")
