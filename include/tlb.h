@@ -86,10 +86,12 @@ typedef struct TlbStatus {
 /* step flags for tlb_fused / tlb_step */
 #define TLB_F_WALL_BOT 1   /* bc rows [Hy, Hy+3) at Twall_bot before collide  */
 #define TLB_F_WALL_TOP 2   /* bc rows [Hy+Ly-3, Hy+Ly) at Twall_top            */
-#define TLB_F_CLAMP_Y 4    /* read Y halo as the wall-row extension (runtime.py:296-305) */
+#define TLB_F_CLAMP_BOT 4  /* read the bottom Y halo as the wall-row extension (runtime.py:296-305) */
 #define TLB_F_WRAP_X 8     /* read X halo periodically (self ring, Np = 1)     */
 #define TLB_F_WRAP_Y 16    /* read Y halo periodically (periodic_y)            */
 #define TLB_F_COUNT_NEG 32 /* add count of written f<0 to status->negatives    */
+#define TLB_F_CLAMP_TOP 64 /* read the top Y halo as the wall-row extension    */
+#define TLB_F_CLAMP_Y (TLB_F_CLAMP_BOT | TLB_F_CLAMP_TOP)
 
 /* library */
 int tlb_version(void);
@@ -167,11 +169,21 @@ int tlb_extend_walls(const TlbField *f, int upper, int lower,
  * runtime.py:199-224 (plans runtime.py:94-107): for d = 1..3, for l with
  * sign*c_l,x >= d in ascending l, one full-height column of NY values.
  * ymode selects how Y-halo rows are sourced when packing: 0 = memory as is
- * (the reference), 1 = wall extension (clamp), 2 = periodic wrap. */
+ * (the reference), 1 = wall extension (clamp) at both walls, 2 = periodic
+ * wrap, 3 = clamp the bottom only, 4 = clamp the top only (2-D wall ranks). */
 int64_t tlb_face_payload_len(const TlbField *f); /* 26 * NY */
 int tlb_pack_x(const TlbField *f, int sign, int ymode, double *buf,
                tlb_stream_t stream);
 int tlb_unpack_x(const TlbField *f, int sign, const double *buf,
+                 tlb_stream_t stream);
+
+/* Face-plan Y payloads (2-D tiling) replace RankWorker.pack_y / unpack_y,
+ * runtime.py:226-246: for e = 1..3, for l with sign*c_l,y >= e in ascending
+ * l, the row Hy+Ly-e (sign +1) or Hy+e-1 (sign -1) over the Lx physical
+ * columns; unpack writes row Hy-e (+1, from below) or Hy+Ly-1+e (-1). */
+int64_t tlb_face_payload_len_y(const TlbField *f); /* 26 * Lx */
+int tlb_pack_y(const TlbField *f, int sign, double *buf, tlb_stream_t stream);
+int tlb_unpack_y(const TlbField *f, int sign, const double *buf,
                  tlb_stream_t stream);
 
 /* pbc_c / pbc_nc with the rank as its own neighbour (1-D ring of one rank;
@@ -198,6 +210,14 @@ int tlb_nccl_unique_id(char *out128);
 int tlb_ring_create(const char *uid128, int nranks, int rank, int device,
                     tlb_ring_t *out);
 int tlb_ring_destroy(tlb_ring_t ring);
+/* 2-D tiling (decompose, runtime.py:54-91): neighbour ranks in the NCCL
+ * communicator; -1 = none (wall side).  With up/down neighbours the step
+ * exchanges Y faces first (physical columns), then X faces (full height, so
+ * corner halos carry diagonal data, runtime.py:8-12).  ybuf holds the two
+ * Y payloads (tlb_face_payload_len_y each) for sending and two for
+ * receiving: 4 * 26 * Lx doubles. */
+int tlb_ring_set_neighbors(tlb_ring_t ring, int left, int right, int up,
+                           int down, double *ybuf);
 /* pack both X faces of f (ymode as tlb_pack_x), exchange with the ring
  * neighbours, unpack into the X halo columns; sbuf/rbuf hold 2 payloads
  * (tlb_face_payload_len each, +x face first). */

@@ -23,8 +23,9 @@ TLB_OK, TLB_ERR_CONTRACT, TLB_ERR_CUDA, TLB_ERR_STENCIL, TLB_ERR_UNSUPPORTED, \
 
 ST_DEGENERATE, ST_SHIFT, ST_EQ_DOMAIN = 1, 2, 4
 
-F_WALL_BOT, F_WALL_TOP, F_CLAMP_Y, F_WRAP_X, F_WRAP_Y, F_COUNT_NEG = \
-    1, 2, 4, 8, 16, 32
+F_WALL_BOT, F_CLAMP_BOT, F_WALL_TOP, F_WRAP_X, F_WRAP_Y, F_COUNT_NEG, F_CLAMP_TOP = \
+    1, 4, 2, 8, 16, 32, 64
+F_CLAMP_Y = F_CLAMP_BOT | F_CLAMP_TOP
 
 ARITH = {"exact": 0, "fast": 1}
 
@@ -83,6 +84,9 @@ SIGNATURES = [
     ("tlb_face_payload_len", _I64, [_FP]),
     ("tlb_pack_x", _INT, [_FP, _INT, _INT, _P, _P]),
     ("tlb_unpack_x", _INT, [_FP, _INT, _P, _P]),
+    ("tlb_face_payload_len_y", _I64, [_FP]),
+    ("tlb_pack_y", _INT, [_FP, _INT, _P, _P]),
+    ("tlb_unpack_y", _INT, [_FP, _INT, _P, _P]),
     ("tlb_pbc_self_x", _INT, [_FP, _P]),
     ("tlb_pbc_self_y", _INT, [_FP, _P]),
     ("tlb_halo_from_peers", _INT, [_FP, _FP, _FP, _P]),
@@ -90,6 +94,7 @@ SIGNATURES = [
     ("tlb_nccl_unique_id", _INT, [ctypes.c_char_p]),
     ("tlb_ring_create", _INT, [ctypes.c_char_p, _INT, _INT, _INT, ctypes.POINTER(_P)]),
     ("tlb_ring_destroy", _INT, [_P]),
+    ("tlb_ring_set_neighbors", _INT, [_P, _INT, _INT, _INT, _INT, _P]),
     ("tlb_ring_exchange", _INT, [_P, _FP, _INT, _P, _P, _P]),
     ("tlb_ring_step", _INT, [_P, _FP, _FP, _PP, _INT, _P, _P, _P, _P, _P, _P]),
     ("tlb_pgm_image", _INT, [_P, _I64, _I64, _I64, _P, _P, _P]),

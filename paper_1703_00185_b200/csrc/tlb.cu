@@ -159,8 +159,9 @@ __device__ __forceinline__ int src_y(int y, int cy, const Fld &s, int flags) {
     if (flags & TLB_F_WRAP_Y) {
         if (ys < s.Hy) ys += s.Ly;
         else if (ys >= s.Hy + s.Ly) ys -= s.Ly;
-    } else if (flags & TLB_F_CLAMP_Y) {
-        ys = ys < s.Hy ? s.Hy : (ys >= s.Hy + s.Ly ? s.Hy + s.Ly - 1 : ys);
+    } else {
+        if ((flags & TLB_F_CLAMP_BOT) && ys < s.Hy) ys = s.Hy;
+        if ((flags & TLB_F_CLAMP_TOP) && ys >= s.Hy + s.Ly) ys = s.Hy + s.Ly - 1;
     }
     return ys;
 }
@@ -472,10 +473,10 @@ static void split_region(SiteLaunch &L, TlbRegion r, const TlbField *f, int flag
         px0 = px0 > f->Hx + h ? px0 : f->Hx + h;
         px1 = px1 < f->Hx + f->Lx - h ? px1 : f->Hx + f->Lx - h;
     }
-    if (flags & (TLB_F_WRAP_Y | TLB_F_CLAMP_Y | TLB_F_WALL_BOT | TLB_F_WALL_TOP)) {
+    if (flags & (TLB_F_WRAP_Y | TLB_F_CLAMP_BOT | TLB_F_WALL_BOT))
         py0 = py0 > f->Hy + h ? py0 : f->Hy + h;
+    if (flags & (TLB_F_WRAP_Y | TLB_F_CLAMP_TOP | TLB_F_WALL_TOP))
         py1 = py1 < f->Hy + f->Ly - h ? py1 : f->Hy + f->Ly - h;
-    }
     if (px1 <= px0 || py1 <= py0) {
         fill_region_edge(L, r);
         return;
@@ -535,9 +536,32 @@ static FaceLines face_lines(int sign, int axis) {
 }
 
 __device__ __forceinline__ int ysrc_mode(int y, const Fld &f, int ymode) {
-    if (ymode == 1) return y < f.Hy ? f.Hy : (y >= f.Hy + f.Ly ? f.Hy + f.Ly - 1 : y);
     if (ymode == 2) return y < f.Hy ? y + f.Ly : (y >= f.Hy + f.Ly ? y - f.Ly : y);
+    if ((ymode == 1 || ymode == 3) && y < f.Hy) return f.Hy;
+    if ((ymode == 1 || ymode == 4) && y >= f.Hy + f.Ly) return f.Hy + f.Ly - 1;
     return y;
+}
+
+// pack_y (runtime.py:226-235): buf[k*Lx + xi] = f[l_k, Hx+xi, row(e_k)]
+__global__ void k_pack_y(Fld f, FaceLines t, int sign, double *buf) {
+    const int k = blockIdx.y;
+    const int xi = blockIdx.x * blockDim.x + threadIdx.x;
+    if (xi >= f.Lx || k >= t.n) return;
+    const int e = t.d[k];
+    const int row = sign == 1 ? f.Hy + f.Ly - e : f.Hy + e - 1;
+    buf[(long long)k * f.Lx + xi] =
+        f.base[(long long)t.l[k] * f.sl + (long long)(f.Hx + xi) * f.sx + (long long)row * f.sy];
+}
+
+// unpack_y (runtime.py:237-246): sign +1 came from below -> rows Hy-e
+__global__ void k_unpack_y(Fld f, FaceLines t, int sign, const double *buf) {
+    const int k = blockIdx.y;
+    const int xi = blockIdx.x * blockDim.x + threadIdx.x;
+    if (xi >= f.Lx || k >= t.n) return;
+    const int e = t.d[k];
+    const int row = sign == 1 ? f.Hy - e : f.Hy + f.Ly - 1 + e;
+    f.base[(long long)t.l[k] * f.sl + (long long)(f.Hx + xi) * f.sx + (long long)row * f.sy] =
+        buf[(long long)k * f.Lx + xi];
 }
 
 // pack_x (runtime.py:199-208): buf[k*NY + y] = f[l_k, col(d_k), y]
@@ -945,6 +969,26 @@ int tlb_unpack_x(const TlbField *f, int sign, const double *buf, tlb_stream_t st
     dim3 grid((NY + 127) / 128, t.n);
     k_unpack_x<<<grid, 128, 0, (cudaStream_t)stream>>>(mkfld(f), t, sign, buf);
     return launch_check("unpack_x");
+}
+
+int64_t tlb_face_payload_len_y(const TlbField *f) {
+    return (int64_t)face_lines(1, 1).n * f->Lx;
+}
+
+int tlb_pack_y(const TlbField *f, int sign, double *buf, tlb_stream_t stream) {
+    if (sign != 1 && sign != -1) return fail(TLB_ERR_CONTRACT, "sign must be +-1");
+    FaceLines t = face_lines(sign, 1);
+    dim3 grid((f->Lx + 127) / 128, t.n);
+    k_pack_y<<<grid, 128, 0, (cudaStream_t)stream>>>(mkfld(f), t, sign, buf);
+    return launch_check("pack_y");
+}
+
+int tlb_unpack_y(const TlbField *f, int sign, const double *buf, tlb_stream_t stream) {
+    if (sign != 1 && sign != -1) return fail(TLB_ERR_CONTRACT, "sign must be +-1");
+    FaceLines t = face_lines(sign, 1);
+    dim3 grid((f->Lx + 127) / 128, t.n);
+    k_unpack_y<<<grid, 128, 0, (cudaStream_t)stream>>>(mkfld(f), t, sign, buf);
+    return launch_check("unpack_y");
 }
 
 int tlb_pbc_self_x(const TlbField *f, tlb_stream_t stream) {

@@ -1,13 +1,16 @@
-// tlb_ring.cuh -- 1-D X ring step across GPUs (one process per GPU).
+// tlb_ring.cuh -- halo-exchange step across GPUs (one process per GPU):
+// the 1-D X ring and the 2-D grid of the reference (decompose,
+// runtime.py:54-91).
 //
-// Replaces RankWorker.pbc_c + the overlapped schedule of RankWorker.step
-// (runtime.py:269-284, 378-396) for ranks on different GPUs.  One call
-// enqueues a whole time step with no host synchronisation:
+// Replaces RankWorker.pbc_nc/pbc_c + the overlapped schedule of
+// RankWorker.step (runtime.py:248-284, 378-396) for ranks on different GPUs.
+// One call enqueues a whole time step with no host synchronisation:
 //
-//   main stream : pack both X faces --ev_pack--> bulk fused kernel  ...wait ev_done
-//   side stream : wait ev_pack; ncclGroup{send+,recv+,send-,recv-};
-//                 unpack both halos; fused kernel on the 3+3 border columns;
-//                 record ev_done
+//   main stream : --ev_pack--> bulk fused kernel ......................... wait ev_done
+//   side stream : wait ev_pack; [2-D: pack Y faces, ncclGroup{Y}, unpack Y];
+//                 pack X faces (full height: corners carry diagonal data);
+//                 ncclGroup{send+,recv+,send-,recv-}; unpack X halos;
+//                 fused kernel on the frame bands; record ev_done
 //
 // The side stream has the highest priority, so the NCCL kernel and the
 // border blocks are dispatched into SM slots as bulk CTAs retire: the
@@ -67,6 +70,8 @@ static Nccl &nccl() {
 struct TlbRing {
     ncclComm_t comm = nullptr;
     int nranks = 0, rank = 0, left = 0, right = 0, device = 0;
+    int up = -1, down = -1;   // 2-D tiling: Y neighbours (-1: wall side)
+    double *ybuf = nullptr;   // 4 Y payloads: send up, send down, from down, from up
     cudaStream_t side = nullptr;
     cudaEvent_t ev_pack = nullptr, ev_done = nullptr;
 };
@@ -126,6 +131,27 @@ static int ring_unpack(const TlbField *f, const double *rbuf, cudaStream_t s) {
     dim3 grid((NY + 127) / 128, tp.n + tm.n);
     k_unpack2<<<grid, 128, 0, s>>>(mkfld(f), tp, tm, rbuf, tp.n * NY);
     return launch_check("ring unpack");
+}
+
+// Y faces (pbc_nc, runtime.py:248-267): rows of physical columns travel up
+// and down; the group order pairs each send with the matching receive even
+// when up == down (two ranks on a periodic Y ring).
+static int ring_exchange_y(TlbRing *r, const TlbField *f, cudaStream_t s) {
+    auto &N = tlbring::nccl();
+    const size_t n = (size_t)tlb_face_payload_len_y(f);
+    double *s_up = r->ybuf, *s_dn = r->ybuf + n, *r_dn = r->ybuf + 2 * n, *r_up = r->ybuf + 3 * n;
+    int e;
+    if (r->up >= 0 && (e = tlb_pack_y(f, 1, s_up, s))) return e;
+    if (r->down >= 0 && (e = tlb_pack_y(f, -1, s_dn, s))) return e;
+    TLB_NCCL_CHECK(N.GroupStart());
+    if (r->up >= 0) TLB_NCCL_CHECK(N.Send(s_up, n, ncclFloat64, r->up, r->comm, s));
+    if (r->down >= 0) TLB_NCCL_CHECK(N.Recv(r_dn, n, ncclFloat64, r->down, r->comm, s));
+    if (r->down >= 0) TLB_NCCL_CHECK(N.Send(s_dn, n, ncclFloat64, r->down, r->comm, s));
+    if (r->up >= 0) TLB_NCCL_CHECK(N.Recv(r_up, n, ncclFloat64, r->up, r->comm, s));
+    TLB_NCCL_CHECK(N.GroupEnd());
+    if (r->down >= 0 && (e = tlb_unpack_y(f, 1, r_dn, s))) return e;
+    if (r->up >= 0 && (e = tlb_unpack_y(f, -1, r_up, s))) return e;
+    return TLB_OK;
 }
 
 static int ring_exchange(TlbRing *r, size_t n_per, const double *sbuf, double *rbuf,
@@ -199,10 +225,26 @@ int tlb_ring_destroy(tlb_ring_t r) {
     return TLB_OK;
 }
 
+int tlb_ring_set_neighbors(tlb_ring_t r, int left, int right, int up, int down, double *ybuf) {
+    if (!r) return fail(TLB_ERR_CONTRACT, "null ring");
+    const int n = r->nranks;
+    if (left < 0 || left >= n || right < 0 || right >= n || up >= n || down >= n)
+        return fail(TLB_ERR_CONTRACT, "neighbour rank out of range");
+    if ((up >= 0 || down >= 0) && !ybuf)
+        return fail(TLB_ERR_CONTRACT, "Y neighbours need a Y payload buffer");
+    r->left = left;
+    r->right = right;
+    r->up = up < 0 ? -1 : up;
+    r->down = down < 0 ? -1 : down;
+    r->ybuf = ybuf;
+    return TLB_OK;
+}
+
 int tlb_ring_exchange(tlb_ring_t r, const TlbField *f, int ymode, double *sbuf, double *rbuf,
                       tlb_stream_t stream) {
     cudaStream_t s = (cudaStream_t)stream;
     int e;
+    if ((r->up >= 0 || r->down >= 0) && (e = ring_exchange_y(r, f, s))) return e;
     if ((e = ring_pack(f, ymode, sbuf, s))) return e;
     const size_t n_per = (size_t)tlb_face_payload_len(f);
     if ((e = ring_exchange(r, n_per, sbuf, rbuf, s))) return e;
@@ -219,22 +261,29 @@ int tlb_ring_step(tlb_ring_t r, const TlbField *prv, const TlbField *nxt, const 
         return fail(TLB_ERR_CONTRACT, "ring step: X halos come from the neighbours");
     cudaStream_t s = (cudaStream_t)stream;
     const int h = TLB_WALL_ROWS;
-    const int ymode = (flags & TLB_F_CLAMP_Y) ? 1 : (flags & TLB_F_WRAP_Y) ? 2 : 0;
-    // 1. faces out of prv (Y halos sourced as the reference's pack would see them)
-    if ((e = ring_pack(prv, ymode, sbuf, s))) return e;
+    const bool cb = (flags & TLB_F_CLAMP_BOT) != 0, ct = (flags & TLB_F_CLAMP_TOP) != 0;
+    const int ymode = (cb && ct) ? 1 : (flags & TLB_F_WRAP_Y) ? 2 : cb ? 3 : ct ? 4 : 0;
+    const bool has_y = r->up >= 0 || r->down >= 0;
+    // Y sides that need the exchange (not walls, not periodic self-wrap)
+    const bool ex_bot = has_y && r->down >= 0, ex_top = has_y && r->up >= 0;
+    // 1. everything that reads prv's faces waits for prv on the side stream
     TLB_CUDA_CHECK(cudaEventRecord(r->ev_pack, s));
     TLB_CUDA_CHECK(cudaStreamWaitEvent(r->side, r->ev_pack, 0));
-    // 2. exchange on the side stream
+    // 2. Y faces first (2-D), then X faces carrying the Y halo rows
+    if (has_y && (e = ring_exchange_y(r, prv, r->side))) return e;
+    if ((e = ring_pack(prv, ymode, sbuf, r->side))) return e;
     const size_t n_per = (size_t)tlb_face_payload_len(prv);
     if ((e = ring_exchange(r, n_per, sbuf, rbuf, r->side))) return e;
-    // 3. bulk columns on the main stream, concurrent with the exchange
+    // 3. bulk on the main stream, concurrent with the exchanges: all columns
+    //    >= 3 from the X edges, all rows not within 3 of an exchanged Y edge
     if (ev_bulk0) TLB_CUDA_CHECK(cudaEventRecord((cudaEvent_t)ev_bulk0, s));
-    if (prv->Lx > 2 * h) {
-        TlbRegion bulk = {prv->Hx + h, prv->Hx + prv->Lx - h, prv->Hy, prv->Hy + prv->Ly};
+    const int by0 = prv->Hy + (ex_bot ? h : 0), by1 = prv->Hy + prv->Ly - (ex_top ? h : 0);
+    if (prv->Lx > 2 * h && by1 > by0) {
+        TlbRegion bulk = {prv->Hx + h, prv->Hx + prv->Lx - h, by0, by1};
         if ((e = tlb_fused(prv, nxt, bulk, p, flags, status, s))) return e;
     }
     if (ev_bulk1) TLB_CUDA_CHECK(cudaEventRecord((cudaEvent_t)ev_bulk1, s));
-    // 4. halos in, then the 3+3 border columns (one launch) on the side stream
+    // 4. halos in, then the frame bands (one launch) on the side stream
     if ((e = ring_unpack(prv, rbuf, r->side))) return e;
     {
         SiteLaunch L;
@@ -247,13 +296,24 @@ int tlb_ring_step(tlb_ring_t r, const TlbField *prv, const TlbField *nxt, const 
         L.step = -1;
         wall_rows(L, prv, flags);
         L.in = mkrect(0, 0, 0, 0);
-        const int wl = prv->Lx > 2 * h ? h : prv->Lx;
-        Rect rs[2] = {mkrect(prv->Hx, prv->Hx + wl, prv->Hy, prv->Hy + prv->Ly),
-                      mkrect(prv->Hx + prv->Lx - h, prv->Hx + prv->Lx, prv->Hy,
-                             prv->Hy + prv->Ly)};
-        set_frames(L, rs, prv->Lx > 2 * h ? 2 : 1);
+        const int x0 = prv->Hx, x1 = prv->Hx + prv->Lx, y0 = prv->Hy, y1 = prv->Hy + prv->Ly;
+        Rect rs[4];
+        int nr = 0;
+        if (prv->Lx > 2 * h) {
+            rs[nr++] = mkrect(x0, x0 + h, y0, y1);
+            rs[nr++] = mkrect(x1 - h, x1, y0, y1);
+            if (by1 > by0) {
+                if (ex_bot) rs[nr++] = mkrect(x0 + h, x1 - h, y0, by0);
+                if (ex_top) rs[nr++] = mkrect(x0 + h, x1 - h, by1, y1);
+            } else {
+                rs[nr++] = mkrect(x0 + h, x1 - h, y0, y1);
+            }
+        } else {
+            rs[nr++] = mkrect(x0, x1, y0, y1);
+        }
+        set_frames(L, rs, nr);
         if ((e = launch_site<K_FUSED, false>(L, p->arith == TLB_ARITH_EXACT, p->order, r->side,
-                                             "ring borders")))
+                                             "ring frames")))
             return e;
     }
     // 5. join

@@ -13,14 +13,15 @@ meaning.  What changes is the machinery under them:
   ranks sit on different GPUs) or ``DistFabric`` (one process per GPU,
   torch.distributed point-to-point over NCCL/NVLink; gloo for the CPU tests);
 * schedule "staged" is the reference's split path, op for op (extend walls,
-  pbc, propagate, bc, collide) -- bitwise the reference, 1184 B/site;
+  pbc_nc, pbc_c, propagate, bc, collide) -- bitwise the reference, 1184 B/site;
   schedule "overlapped" is the B200 path: one fused propagate+bc+collide
-  kernel per region with the wall extension and (for a single rank) the
-  periodic X wrap folded into its loads, the X-face exchange overlapped with
-  the bulk columns on a side stream, then the 3+3 border columns -- 592 B/site.
+  kernel per region with the wall extension and the periodic wraps of a rank
+  that is its own neighbour folded into its loads, the face exchanges (Y
+  first, then X over the full height) on a high-priority side stream
+  overlapped with the bulk, then the frame bands -- 592 B/site.
 
-2-D tilings (Y exchange, pbc_nc between ranks) are outside this round's
-scope: ``RankWorker`` raises UnsupportedCaseError for them.
+Both decompositions of the reference are supported: the 1-D X ring (the
+north star) and the 2-D grid (Y chain with walls or Y ring).
 """
 
 import math
@@ -166,25 +167,40 @@ class Fabric:
             self.failures.append((rank, exc))
         self.abort.set()
 
-    # -- X-face exchange used by RankWorker -------------------------------
-    def start_x(self, w, step, out_plus, out_minus):
+    # -- face exchange used by RankWorker ---------------------------------
+    # axis "x": +face -> right ("x+"), -face -> left ("x-"); received +face
+    # comes from the left.  axis "y": +face -> up ("y+"), -face -> down
+    # ("y-"); received +face comes from below.  Wall sides (no neighbour)
+    # send and receive nothing (runtime.py:248-284).
+    @staticmethod
+    def _peers(w, axis):
+        nb = w.tile.neighbors
+        return (nb["right"], nb["left"]) if axis == "x" else (nb["up"], nb["down"])
+
+    def start_face(self, w, step, axis, out_plus, out_minus):
         torch = _lib.torch_cuda()
         ev = torch.cuda.Event()
-        ev.record(w.stream)
-        nb = w.tile.neighbors
-        self.send(w.tile.rank, nb["right"], "x+", step, out_plus, ev)
-        self.send(w.tile.rank, nb["left"], "x-", step, out_minus, ev)
+        ev.record(torch.cuda.current_stream(w.device))
+        fwd, bwd = self._peers(w, axis)
+        if fwd is not None:
+            self.send(w.tile.rank, fwd, axis + "+", step, out_plus, ev)
+        if bwd is not None:
+            self.send(w.tile.rank, bwd, axis + "-", step, out_minus, ev)
         return step
 
-    def finish_x(self, w, handle, in_plus, in_minus, stream=None):
+    def finish_face(self, w, handle, axis, in_plus, in_minus, stream=None):
         torch = _lib.torch_cuda()
         stream = stream or w.stream
         step = handle
-        nb = w.tile.neighbors
-        for tag, src, dst in (("x+", nb["left"], in_plus), ("x-", nb["right"], in_minus)):
+        fwd, bwd = self._peers(w, axis)
+        got = []
+        for tag, src, dst in ((axis + "+", bwd, in_plus), (axis + "-", fwd, in_minus)):
+            if src is None:
+                got.append(False)
+                continue
             payload, ev = self.recv(w.tile.rank, src, tag, step, with_event=True)
             if payload.numel() != dst.numel():
-                raise ProtocolError(f"rank {w.tile.rank}: X payload size mismatch")
+                raise ProtocolError(f"rank {w.tile.rank}: {axis.upper()} payload size mismatch")
             if ev is not None:
                 stream.wait_event(ev)
             with torch.cuda.stream(stream):
@@ -193,6 +209,14 @@ class Fabric:
                 payload.record_stream(stream)
             else:
                 w.retain(payload)  # peer copy: keep alive until the next sync
+            got.append(True)
+        return got
+
+    def start_x(self, w, step, out_plus, out_minus):
+        return self.start_face(w, step, "x", out_plus, out_minus)
+
+    def finish_x(self, w, handle, in_plus, in_minus, stream=None):
+        return self.finish_face(w, handle, "x", in_plus, in_minus, stream)
 
 
 class DistFabric:
@@ -242,23 +266,44 @@ class DistFabric:
             _lib.load().tlb_ring_destroy(self._ring)
             self._ring = None
 
-    def start_x(self, w, step, out_plus, out_minus):
+    def start_face(self, w, step, axis, out_plus, out_minus):
         dist = self.dist
         nb = w.tile.neighbors
-        ops = [dist.P2POp(dist.isend, out_plus, nb["right"], self.group),
-               dist.P2POp(dist.isend, out_minus, nb["left"], self.group),
-               dist.P2POp(dist.irecv, w.rbuf_plus, nb["left"], self.group),
-               dist.P2POp(dist.irecv, w.rbuf_minus, nb["right"], self.group)]
-        return dist.batch_isend_irecv(ops)
+        if axis == "x":
+            fwd, bwd = nb["right"], nb["left"]
+            rin_p, rin_m = w.rbuf_plus, w.rbuf_minus
+        else:
+            fwd, bwd = nb["up"], nb["down"]
+            rin_p, rin_m = w.rbuf_y_plus, w.rbuf_y_minus
+        # same op order on every rank: each send is matched by the peer's
+        # receive of the same direction, also when fwd == bwd
+        ops = []
+        if fwd is not None:
+            ops.append(dist.P2POp(dist.isend, out_plus, fwd, self.group))
+        if bwd is not None:
+            ops.append(dist.P2POp(dist.irecv, rin_p, bwd, self.group))
+        if bwd is not None:
+            ops.append(dist.P2POp(dist.isend, out_minus, bwd, self.group))
+        if fwd is not None:
+            ops.append(dist.P2POp(dist.irecv, rin_m, fwd, self.group))
+        return (dist.batch_isend_irecv(ops) if ops else []), (bwd is not None, fwd is not None)
 
-    def finish_x(self, w, handle, in_plus, in_minus, stream=None):
+    def finish_face(self, w, handle, axis, in_plus, in_minus, stream=None):
         # called under torch.cuda.stream(stream): wait() orders it after NCCL
-        for req in handle:
+        reqs, got = handle
+        for req in reqs:
             try:
                 req.wait()
             except Exception as exc:  # timeouts surface as DeadlockError
-                raise DeadlockError(f"rank {w.tile.rank} stalled in the X exchange: {exc}",
-                                    rank=w.tile.rank) from exc
+                raise DeadlockError(f"rank {w.tile.rank} stalled in the {axis.upper()} "
+                                    f"exchange: {exc}", rank=w.tile.rank) from exc
+        return list(got)
+
+    def start_x(self, w, step, out_plus, out_minus):
+        return self.start_face(w, step, "x", out_plus, out_minus)
+
+    def finish_x(self, w, handle, in_plus, in_minus, stream=None):
+        return self.finish_face(w, handle, "x", in_plus, in_minus, stream)
 
     def fail(self, rank, exc):
         self.failures.append((rank, exc))
@@ -279,16 +324,19 @@ class RankWorker:
     (runtime.py:163-404).
 
     ``fabric`` is a ``Fabric`` (in-process ranks) or ``DistFabric`` (one
-    process per GPU).  ``device`` selects the GPU (default: current)."""
+    process per GPU).  ``device`` selects the GPU (default: current).  Both
+    the 1-D X ring and the 2-D grid of ``decompose`` are supported; a step is
+    three phases (``step_begin``/``step_mid``/``step_end``) so in-process
+    ranks can be driven in lock step: Y faces are exchanged before X faces,
+    whose full-height columns then carry the diagonal corners
+    (runtime.py:8-12)."""
+
+    _RING = 1024
 
     def __init__(self, tile, vs, params, fabric=None, schedule="staged", walls=True,
                  layout="soa", halo=DEFAULT_HALO, debug_poison=False, device=None,
                  periodic_y=False):
         torch = _lib.torch_cuda()
-        if tile.grid[1] != 1:
-            raise UnsupportedCaseError(
-                "2-D tilings (Y exchange between ranks) are not built in this round; "
-                "use tiling='1d'")
         if schedule not in ("staged", "overlapped"):
             raise ConfigurationError(f"unknown schedule {schedule!r}")
         self.tile = tile
@@ -303,20 +351,40 @@ class RankWorker:
             "cuda", torch.cuda.current_device())
         self.geom = LatticeGeometry(tile.Lx, tile.Ly, halo, halo, vs.Q, layout)
         self.halo = halo
+        nb = tile.neighbors
+        self.x_self = nb["left"] == tile.rank
+        # Y: ring onto itself (one row of ranks, periodic), or exchange with
+        # up/down neighbours (2-D), or walls
+        self.y_self = tile.grid[1] == 1 and nb["up"] is not None
+        self.ex_up = nb["up"] is not None and not self.y_self
+        self.ex_down = nb["down"] is not None and not self.y_self
+        self.y_exchange = self.ex_up or self.ex_down
+        self.wall_bot = walls and tile.lowermost
+        self.wall_top = walls and tile.uppermost
         with torch.cuda.device(self.device):
             _lib.ensure_stencil(vs, self.device.index)
             self.prv, self.nxt = allocate_field(self.geom, vs, device=self.device)
             self.stream = torch.cuda.Stream(self.device)
             self.comm_stream = torch.cuda.Stream(self.device, priority=-1)
-            n = int(_lib.load().tlb_face_payload_len(field_desc(self.prv)))
-            self.payload_len = n
+            lib = _lib.load()
+            n = int(lib.tlb_face_payload_len(field_desc(self.prv)))
+            ny_ = int(lib.tlb_face_payload_len_y(field_desc(self.prv)))
+            self.payload_len, self.payload_len_y = n, ny_
             self.rbuf_plus = torch.empty(n, dtype=torch.float64, device=self.device)
             self.rbuf_minus = torch.empty(n, dtype=torch.float64, device=self.device)
+            self.rbuf_y_plus = torch.empty(ny_, dtype=torch.float64, device=self.device)
+            self.rbuf_y_minus = torch.empty(ny_, dtype=torch.float64, device=self.device)
             self._ring = None
-            if isinstance(fabric, DistFabric) and fabric.native and tile.grid[0] > 1:
+            if isinstance(fabric, DistFabric) and fabric.native and fabric.Np > 1:
+                import ctypes
                 self._ring = fabric.ring(self.device.index)
                 self.sbuf2 = torch.empty(2 * n, dtype=torch.float64, device=self.device)
                 self.rbuf2 = torch.empty(2 * n, dtype=torch.float64, device=self.device)
+                self.ybuf4 = torch.empty(4 * ny_, dtype=torch.float64, device=self.device)
+                _lib.check(lib.tlb_ring_set_neighbors(
+                    self._ring, nb["left"], nb["right"],
+                    nb["up"] if self.ex_up else -1, nb["down"] if self.ex_down else -1,
+                    ctypes.c_void_p(self.ybuf4.data_ptr())), "ring neighbours")
             self._status_ring = torch.zeros((self._RING, _lib.STATUS_BYTES),
                                             dtype=torch.uint8, device=self.device)
             # order the allocations' zero-fills before any work on our stream
@@ -331,34 +399,42 @@ class RankWorker:
     # -- helpers -------------------------------------------------------------
     @property
     def Np(self):
-        return self.tile.grid[0]
+        return self.tile.grid[0] * self.tile.grid[1]
 
     @property
     def self_ring(self):
-        return self.tile.neighbors["left"] == self.tile.rank
+        return self.x_self
 
-    def _sp(self):
-        return self.stream.cuda_stream
+    def _sp(self, stream=None):
+        return (stream or self.stream).cuda_stream
 
     def _check(self, code, what):
         _lib.check(code, what)
 
-    def _wall_flags(self):
-        f = 0
-        if self.walls and self.tile.lowermost:
-            f |= _lib.F_WALL_BOT
-        if self.walls and self.tile.uppermost:
-            f |= _lib.F_WALL_TOP
+    def _flags(self):
+        """Fused-kernel flags of this rank (walls, implicit halos, monitor)."""
+        f = _lib.F_COUNT_NEG
+        if self.wall_bot:
+            f |= _lib.F_WALL_BOT | _lib.F_CLAMP_BOT
+        if self.wall_top:
+            f |= _lib.F_WALL_TOP | _lib.F_CLAMP_TOP
+        if self.y_self:
+            f |= _lib.F_WRAP_Y
+        if self.x_self:
+            f |= _lib.F_WRAP_X
         return f
 
     def _ymode(self):
-        if self.walls:
+        """How pack_x sources the Y halo rows (tlb_pack_x)."""
+        if self.wall_bot and self.wall_top:
             return 1
-        if self.periodic_y:
+        if self.y_self:
             return 2
+        if self.wall_bot:
+            return 3
+        if self.wall_top:
+            return 4
         return 0
-
-    _RING = 1024
 
     def _status_slot(self):
         if len(self._records) >= self._RING:
@@ -369,13 +445,13 @@ class RankWorker:
         self._retained.append(t)
 
     # -- halo exchange (reference names) -------------------------------------
-    def pack_x(self, f, sign, ymode=0):
+    def pack_x(self, f, sign, ymode=0, stream=None):
         """Outgoing X-face payload (runtime.py:199-208); a new device tensor."""
         torch = _lib.torch_cuda()
-        with torch.cuda.stream(self.stream):
+        with torch.cuda.stream(stream or self.stream):
             buf = torch.empty(self.payload_len, dtype=torch.float64, device=self.device)
         self._check(_lib.load().tlb_pack_x(field_desc(f), int(sign), int(ymode),
-                                           buf.data_ptr(), self._sp()), "pack_x")
+                                           buf.data_ptr(), self._sp(stream)), "pack_x")
         return buf
 
     def unpack_x(self, f, sign, payload, stream=None):
@@ -385,38 +461,71 @@ class RankWorker:
             payload = torch.as_tensor(np.asarray(payload, dtype=np.float64), device=self.device)
         if payload.numel() != self.payload_len:
             raise ProtocolError(f"rank {self.tile.rank}: X payload size mismatch")
-        sp = (stream or self.stream).cuda_stream
         self._check(_lib.load().tlb_unpack_x(field_desc(f), int(sign), payload.data_ptr(),
-                                             sp), "unpack_x")
+                                             self._sp(stream)), "unpack_x")
+
+    def pack_y(self, f, sign, stream=None):
+        """Outgoing Y-face payload, physical columns only (runtime.py:226-235)."""
+        torch = _lib.torch_cuda()
+        with torch.cuda.stream(stream or self.stream):
+            buf = torch.empty(self.payload_len_y, dtype=torch.float64, device=self.device)
+        self._check(_lib.load().tlb_pack_y(field_desc(f), int(sign), buf.data_ptr(),
+                                           self._sp(stream)), "pack_y")
+        return buf
+
+    def unpack_y(self, f, sign, payload, stream=None):
+        """Scatter a received Y payload into the halo rows (runtime.py:237-246)."""
+        torch = _lib.torch_cuda()
+        if not isinstance(payload, torch.Tensor):
+            payload = torch.as_tensor(np.asarray(payload, dtype=np.float64), device=self.device)
+        if payload.numel() != self.payload_len_y:
+            raise ProtocolError(f"rank {self.tile.rank}: Y payload size mismatch")
+        self._check(_lib.load().tlb_unpack_y(field_desc(f), int(sign), payload.data_ptr(),
+                                             self._sp(stream)), "unpack_y")
+
+    def _start(self, axis, step, f, ymode=0, stream=None):
+        torch = _lib.torch_cuda()
+        stream = stream or self.stream
+        if axis == "x":
+            out = (self.pack_x(f, 1, ymode, stream), self.pack_x(f, -1, ymode, stream))
+        else:
+            out = (self.pack_y(f, 1, stream), self.pack_y(f, -1, stream))
+        with torch.cuda.stream(stream):
+            return self.fabric.start_face(self, step, axis, *out)
+
+    def _finish(self, axis, f, handle, stream=None):
+        torch = _lib.torch_cuda()
+        stream = stream or self.stream
+        bufs = ((self.rbuf_plus, self.rbuf_minus) if axis == "x"
+                else (self.rbuf_y_plus, self.rbuf_y_minus))
+        with torch.cuda.stream(stream):
+            got = self.fabric.finish_face(self, handle, axis, *bufs, stream)
+        unpack = self.unpack_x if axis == "x" else self.unpack_y
+        if got[0]:
+            unpack(f, 1, bufs[0], stream)
+        if got[1]:
+            unpack(f, -1, bufs[1], stream)
+
+    def pbc_nc(self, f, step):
+        """Exchange the Y halo rows (runtime.py:264-267)."""
+        if self.y_self:
+            self._check(_lib.load().tlb_pbc_self_y(field_desc(f), self._sp()), "pbc_nc")
+        elif self.y_exchange:
+            self._finish("y", f, self._start("y", step, f))
 
     def pbc_c(self, f, step):
         """Exchange the X halo columns around the ring (runtime.py:281-284)."""
-        if self.self_ring:
+        if self.x_self:
             self._check(_lib.load().tlb_pbc_self_x(field_desc(f), self._sp()), "pbc_c")
             return
-        h = self._start_exchange(step, self.pack_x(f, 1), self.pack_x(f, -1))
-        self._finish_exchange(f, h)
-
-    def _start_exchange(self, step, out_plus, out_minus):
-        torch = _lib.torch_cuda()
-        with torch.cuda.stream(self.stream):
-            return self.fabric.start_x(self, step, out_plus, out_minus)
-
-    def _finish_exchange(self, f, handle, stream=None):
-        torch = _lib.torch_cuda()
-        stream = stream or self.stream
-        with torch.cuda.stream(stream):
-            self.fabric.finish_x(self, handle, self.rbuf_plus, self.rbuf_minus, stream)
-        self.unpack_x(f, 1, self.rbuf_plus, stream)
-        self.unpack_x(f, -1, self.rbuf_minus, stream)
+        self._finish("x", f, self._start("x", step, f))
 
     def _extend_wall_halos(self, f):
         """runtime.py:296-305."""
-        up = self.walls and self.tile.uppermost
-        lo = self.walls and self.tile.lowermost
-        if up or lo:
-            self._check(_lib.load().tlb_extend_walls(field_desc(f), int(up), int(lo),
-                                                     self._sp()), "extend_walls")
+        if self.wall_top or self.wall_bot:
+            self._check(_lib.load().tlb_extend_walls(field_desc(f), int(self.wall_top),
+                                                     int(self.wall_bot), self._sp()),
+                        "extend_walls")
 
     def _poison_halos(self, f):
         """runtime.py:288-294 (debug mode only)."""
@@ -432,25 +541,48 @@ class RankWorker:
     def _bc_rows(self):
         g = self.geom
         rows = []
-        if self.walls and self.tile.lowermost:
+        if self.wall_bot:
             rows.append((g.Hy, g.Hy + WALL_ROWS))
-        if self.walls and self.tile.uppermost:
+        if self.wall_top:
             rows.append((g.Hy + g.Ly - WALL_ROWS, g.Hy + g.Ly))
         return rows
 
     # -- schedules -----------------------------------------------------------
-    def _fused(self, x0, x1, flags, st, stream=None):
-        g = self.geom
-        if x1 <= x0:
+    def _fused(self, x0, x1, y0, y1, flags, st, stream=None):
+        if x1 <= x0 or y1 <= y0:
             return
-        sp = (stream or self.stream).cuda_stream
         self._check(_lib.load().tlb_fused(
-            field_desc(self.prv), field_desc(self.nxt),
-            _lib.region(x0, x1, g.Hy, g.Hy + g.Ly), self.tparams, flags, st, sp), "fused")
+            field_desc(self.prv), field_desc(self.nxt), _lib.region(x0, x1, y0, y1),
+            self.tparams, flags, st, self._sp(stream)), "fused")
+
+    def _bulk_rect(self):
+        """Sites that need no exchanged halo (RankWorker._frame_slices,
+        runtime.py:326-338): 3 away from exchanged X and Y edges."""
+        g, h = self.geom, self.halo
+        x0, x1 = g.Hx, g.Hx + g.Lx
+        if not self.x_self:
+            x0, x1 = g.Hx + h, max(g.Hx + h, g.Hx + g.Lx - h)
+        y0 = min(g.Hy + (h if self.ex_down else 0), g.Hy + g.Ly)
+        y1 = max(y0, g.Hy + g.Ly - (h if self.ex_up else 0))
+        return x0, x1, y0, y1
+
+    def _frames(self, flags, st, stream):
+        """The bands around the bulk rectangle, after the exchanges."""
+        g = self.geom
+        X0, X1, Y0, Y1 = g.Hx, g.Hx + g.Lx, g.Hy, g.Hy + g.Ly
+        x0, x1, y0, y1 = self._bulk_rect()
+        if x1 <= x0:   # tile narrower than two borders: everything is frame
+            self._fused(X0, X1, Y0, Y1, flags, st, stream)
+            return
+        self._fused(X0, x0, Y0, Y1, flags, st, stream)
+        self._fused(x1, X1, Y0, Y1, flags, st, stream)
+        self._fused(x0, x1, Y0, y0, flags, st, stream)
+        self._fused(x0, x1, y1, Y1, flags, st, stream)
 
     def step(self, step_no):
-        """One time step (runtime.py:355-400), enqueued on the rank's stream."""
+        """One time step (runtime.py:355-400), enqueued on the rank's streams."""
         self.step_begin(step_no)
+        self.step_mid(step_no)
         self.step_end(step_no)
 
     def step_begin(self, step_no):
@@ -461,91 +593,103 @@ class RankWorker:
         st = slot.data_ptr()
         ev = tuple(torch.cuda.Event(enable_timing=True) for _ in range(4))
         self._pending = (step_no, slot, ev, st)
+        self._hy = self._hx = None
+        self._bulk_timed = False
         ev[0].record(self.stream)
         if self.debug_poison:
             self._poison_halos(self.prv)
         if self.schedule == "staged":
-            # reference path, op for op
-            if self.walls:
-                self._extend_wall_halos(self.prv)
-            if self.periodic_y:
-                self._check(lib.tlb_pbc_self_y(field_desc(self.prv), self._sp()), "pbc_nc")
-            if self.self_ring:
-                self._check(lib.tlb_pbc_self_x(field_desc(self.prv), self._sp()), "pbc_c")
-                self._handle = None
-            elif self._ring is not None:
+            # the reference's order: wall extension, Y halos, X halos
+            self._extend_wall_halos(self.prv)
+            if self._ring is not None:
                 self._check(lib.tlb_ring_exchange(
                     self._ring, field_desc(self.prv), 0, self.sbuf2.data_ptr(),
                     self.rbuf2.data_ptr(), self._sp()), "ring exchange")
-                self._handle = None
-            else:
-                self._handle = self._start_exchange(step_no, self.pack_x(self.prv, 1),
-                                                    self.pack_x(self.prv, -1))
-            ev[1].record(self.stream)
+            elif self.y_self:
+                self._check(lib.tlb_pbc_self_y(field_desc(self.prv), self._sp()), "pbc_nc")
+            elif self.y_exchange:
+                self._hy = self._start("y", step_no, self.prv)
             return
-        # overlapped: fused kernels with the wall extension folded in
-        flags = self._wall_flags() | _lib.F_COUNT_NEG
-        if self.walls:
-            flags |= _lib.F_CLAMP_Y
-        elif self.periodic_y:
-            flags |= _lib.F_WRAP_Y
-        self._flags = flags
-        if self.self_ring:
-            ev[1].record(self.stream)
-            self._check(lib.tlb_fused(
-                field_desc(self.prv), field_desc(self.nxt),
-                _lib.region(g.Hx, g.Hx + g.Lx, g.Hy, g.Hy + g.Ly), self.tparams,
-                flags | _lib.F_WRAP_X, st, self._sp()), "fused")
-            self._handle = None
-            return
+        flags = self._flags()
+        self._flags_now = flags
         if self._ring is not None:
             ev[1].record(self.stream)
             ev[2].record(self.stream)
             self._check(lib.tlb_ring_step(
-                self._ring, field_desc(self.prv), field_desc(self.nxt), self.tparams, flags,
-                st, self.sbuf2.data_ptr(), self.rbuf2.data_ptr(), ev[1].cuda_event,
-                ev[2].cuda_event, self._sp()), "ring step")
-            self._handle = None
+                self._ring, field_desc(self.prv), field_desc(self.nxt), self.tparams,
+                flags & ~_lib.F_WRAP_X, st, self.sbuf2.data_ptr(), self.rbuf2.data_ptr(),
+                ev[1].cuda_event, ev[2].cuda_event, self._sp()), "ring step")
+            self._bulk_timed = True
             return
-        h = self.halo
-        ymode = self._ymode()
-        out_p = self.pack_x(self.prv, 1, ymode)
-        out_m = self.pack_x(self.prv, -1, ymode)
-        self._handle = self._start_exchange(step_no, out_p, out_m)
+        if self.x_self and not self.y_exchange:
+            # one fused launch is the whole step (implicit periodic X halo)
+            ev[1].record(self.stream)
+            self._fused(g.Hx, g.Hx + g.Lx, g.Hy, g.Hy + g.Ly, flags, st)
+            ev[2].record(self.stream)
+            self._bulk_timed = True
+            return
+        # faces out on the high-priority side stream (after prv is complete),
+        # bulk on the main stream concurrently
+        cs = self.comm_stream
+        cs.wait_stream(self.stream)
+        if self.y_exchange:
+            self._hy = self._start("y", step_no, self.prv, stream=cs)
+        elif not self.x_self:
+            self._hx = self._start("x", step_no, self.prv, self._ymode(), stream=cs)
         ev[1].record(self.stream)
-        self._fused(g.Hx + h, g.Hx + g.Lx - h, flags, st)   # bulk columns
+        self._fused(*self._bulk_rect(), flags, st)
         ev[2].record(self.stream)
+        self._bulk_timed = True
+
+    def step_mid(self, step_no):
+        """Y halos in, then X faces out (2-D); nothing to do on a 1-D ring."""
+        if self._hy is None:
+            if self.schedule == "staged" and self._ring is None and self._hx is None:
+                if self.x_self:
+                    self._check(_lib.load().tlb_pbc_self_x(field_desc(self.prv), self._sp()),
+                                "pbc_c")
+                else:
+                    self._hx = self._start("x", step_no, self.prv)
+            return
+        stream = self.comm_stream if self.schedule == "overlapped" else self.stream
+        self._finish("y", self.prv, self._hy, stream)
+        self._hy = None
+        if self.x_self:
+            if self.schedule == "staged":
+                self._check(_lib.load().tlb_pbc_self_x(field_desc(self.prv), self._sp()),
+                            "pbc_c")
+            return
+        ymode = 0 if self.schedule == "staged" else self._ymode()
+        self._hx = self._start("x", step_no, self.prv, ymode, stream=stream)
 
     def step_end(self, step_no):
         g = self.geom
         lib = _lib.load()
         step_no_, slot, ev, st = self._pending
         if self.schedule == "staged":
-            if self._handle is not None:
-                self._finish_exchange(self.prv, self._handle)
+            if self._hx is not None:
+                self._finish("x", self.prv, self._hx)
+                self._hx = None
+            ev[1].record(self.stream)
             ev[2].record(self.stream)
             full = _lib.region(g.Hx, g.Hx + g.Lx, g.Hy, g.Hy + g.Ly)
             self._check(lib.tlb_propagate(field_desc(self.prv), field_desc(self.nxt), full,
                                           self._sp()), "propagate")
-            if self.walls and (self.tile.uppermost or self.tile.lowermost):
-                self._check(lib.tlb_bc(field_desc(self.nxt), self.tparams,
-                                       int(self.tile.uppermost), int(self.tile.lowermost),
-                                       g.Hx, g.Hx + g.Lx, st, self._sp()), "bc")
+            if self.wall_top or self.wall_bot:
+                self._check(lib.tlb_bc(field_desc(self.nxt), self.tparams, int(self.wall_top),
+                                       int(self.wall_bot), g.Hx, g.Hx + g.Lx, st, self._sp()),
+                            "bc")
             self._check(lib.tlb_collide(field_desc(self.nxt), field_desc(self.nxt), full,
                                         self.tparams, _lib.F_COUNT_NEG, st, self._sp()),
                         "collide")
-        else:
-            if self._handle is not None:
-                # halo arrival -> unpack -> 3+3 border columns on the
-                # high-priority side stream, concurrent with the bulk kernel
-                cs = self.comm_stream
-                self._finish_exchange(self.prv, self._handle, cs)
-                h = self.halo
-                self._fused(g.Hx, g.Hx + h, self._flags, st, cs)
-                self._fused(g.Hx + g.Lx - h, g.Hx + g.Lx, self._flags, st, cs)
-                self.stream.wait_stream(cs)
-            elif self._ring is None:
-                ev[2].record(self.stream)
+        elif self._ring is None and not (self.x_self and not self.y_exchange):
+            # halos in -> frame bands on the side stream, concurrent with bulk
+            cs = self.comm_stream
+            if self._hx is not None:
+                self._finish("x", self.prv, self._hx, cs)
+                self._hx = None
+            self._frames(self._flags_now, st, cs)
+            self.stream.wait_stream(cs)
         ev[3].record(self.stream)
         self._records.append(_StepRecord(step_no, slot, ev))
         self.prv, self.nxt = swap_buffers(self.prv, self.nxt)
@@ -568,7 +712,7 @@ class RankWorker:
             s = _lib.TlbStatus.from_buffer_copy(row.tobytes())
             t0, t1, t2, t3 = rec.events
             if self.schedule == "staged":
-                m = {"t_comm_nc": 0.0, "t_comm_c": t0.elapsed_time(t2) * 1e-3,
+                m = {"t_comm_nc": 0.0, "t_comm_c": t0.elapsed_time(t1) * 1e-3,
                      "t_bulk": t2.elapsed_time(t3) * 1e-3, "t_border": 0.0}
             else:
                 m = {"t_comm_nc": 0.0, "t_comm_c": t0.elapsed_time(t1) * 1e-3,

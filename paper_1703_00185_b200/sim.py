@@ -140,12 +140,12 @@ def run(cfg: SimConfig, f0=None) -> RunResult:
     t0 = time.perf_counter()
     try:
         for s in range(cfg.steps):
-            for w in workers:
-                with torch.cuda.device(w.device):
-                    w.step_begin(s)
-            for w in workers:
-                with torch.cuda.device(w.device):
-                    w.step_end(s)
+            # lock step over the in-process ranks: every rank's sends are
+            # posted before any rank waits (Y faces, then X faces)
+            for phase in ("step_begin", "step_mid", "step_end"):
+                for w in workers:
+                    with torch.cuda.device(w.device):
+                        getattr(w, phase)(s)
             if cfg.debug_poison:
                 for w in workers:
                     if not bool(torch.isfinite(w.physical_block()).all()):

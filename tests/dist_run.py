@@ -38,16 +38,18 @@ def main():
         f0 = O.equilibrium(*O.rayleigh_taylor_macro(Lx, Ly, vs.cs2))
         want, neg = O.run(f0, steps, O.params6(p.tau, p.gx, p.gy, p.dt, p.Twall_top,
                                                  p.Twall_bot))
+    tilings = ["1d", (1, world)] + ([(2, world // 2)] if world >= 4 else [])
     ok = True
-    for schedule in ("overlapped", "staged"):
-        res = tl.run(tl.SimConfig(Lx=Lx, Ly=Ly, Np=world, steps=steps, params=p,
-                                  init="rayleigh-taylor", schedule=schedule))
-        if rank == 0:
-            same = np.array_equal(res.populations, want)
-            print(f"schedule={schedule} world={world} bitwise={same} "
-                  f"mlups={res.mlups:.1f}", flush=True)
-            ok &= same
-        assert len(res.metrics) == steps
+    for tiling in tilings:
+        for schedule in ("overlapped", "staged"):
+            res = tl.run(tl.SimConfig(Lx=Lx, Ly=Ly, Np=world, tiling=tiling, steps=steps,
+                                      params=p, init="rayleigh-taylor", schedule=schedule))
+            if rank == 0:
+                same = np.array_equal(res.populations, want)
+                print(f"tiling={tiling} schedule={schedule} world={world} bitwise={same} "
+                      f"mlups={res.mlups:.1f}", flush=True)
+                ok &= same
+            assert len(res.metrics) == steps
     dist.barrier()
     if rank == 0:
         print("DIST OK" if ok else "DIST FAIL", flush=True)

@@ -261,9 +261,93 @@ def test_device_output_and_explicit_f0(vs):
     assert np.array_equal(dev.populations.cpu().numpy(), host.populations)
 
 
-def test_two_d_tiling_rejected(vs):
-    with pytest.raises(tl.UnsupportedCaseError):
-        tl.run(tl.SimConfig(Lx=16, Ly=16, Np=4, tiling=(2, 2), steps=1))
+# ------------------------------------------------------------ 2-D tiling --
+
+@pytest.mark.parametrize("tiling,schedule", [((2, 2), "overlapped"), ((2, 2), "staged"),
+                                             ((2, 4), "overlapped"), ((1, 4), "staged"),
+                                             ((4, 2), "overlapped")])
+def test_2d_rank_invariance(vs, tiling, schedule):
+    """test_acceptance.py:106-121 / test_runtime.py:252-260 with 2-D grids:
+    bitwise equal to one rank (walls in Y, periodic X)."""
+    p = tl.PhysicsParams(tau=0.8, gy=-1e-4, Twall_top=0.6, Twall_bot=0.75)
+    kw = dict(Lx=64, Ly=48, model="D2Q37", steps=12, params=p, init="random",
+              init_kwargs={"seed": 5})
+    ref = tl.run(tl.SimConfig(Np=1, schedule="staged", **kw))
+    Np = tiling[0] * tiling[1]
+    res = tl.run(tl.SimConfig(Np=Np, tiling=tiling, schedule=schedule, **kw))
+    assert np.array_equal(res.populations, ref.populations)
+
+
+@pytest.mark.parametrize("schedule", ["overlapped", "staged"])
+def test_2d_periodic_y_invariance(vs, schedule):
+    p = tl.PhysicsParams(tau=0.8, gx=1e-5)
+    kw = dict(Lx=32, Ly=32, steps=10, params=p, walls=False, periodic_y=True,
+              init="random", init_kwargs={"seed": 8})
+    ref = tl.run(tl.SimConfig(Np=1, schedule="staged", **kw))
+    for tiling in ((2, 2), (1, 2), (2, 4)):
+        Np = tiling[0] * tiling[1]
+        res = tl.run(tl.SimConfig(Np=Np, tiling=tiling, schedule=schedule, **kw))
+        assert np.array_equal(res.populations, ref.populations), tiling
+
+
+def test_2d_halo_poisoning(vs):
+    """test_acceptance.py:219-230 with the reference's 2x2 grid."""
+    p = tl.PhysicsParams(tau=0.8, gy=-1e-4, Twall_top=0.6, Twall_bot=0.75)
+    for schedule in ("overlapped", "staged"):
+        res = tl.run(tl.SimConfig(Lx=32, Ly=32, Np=4, tiling=(2, 2), schedule=schedule,
+                                  steps=20, params=p, init="random",
+                                  init_kwargs={"seed": 2}, debug_poison=True))
+        assert np.all(np.isfinite(res.populations))
+
+
+def _workers(vs, Lx, Ly, Np, tiling, periodic_y=False, walls=True):
+    tiles = tl.decompose(Lx, Ly, Np, tiling, periodic_y=periodic_y)
+    fab = tl.Fabric(Np, timeout=5.0)
+    p = tl.PhysicsParams(tau=0.8, Twall_top=0.6, Twall_bot=0.8)
+    return [tl.RankWorker(t, vs, p, fab, walls=walls, periodic_y=periodic_y) for t in tiles]
+
+
+def test_corner_diagonal_via_protocol_order(vs):
+    """test_runtime.py:161-185: Y exchange first, then X over the full
+    height, so a corner sentinel from the diagonal neighbour arrives."""
+    ws = _workers(vs, 8, 8, 4, (2, 2), periodic_y=True, walls=False)
+    l = vs.find(-1, -1)
+    g = ws[0].geom
+    ws[3].prv.pops[l, g.Hx, g.Hy] = 7.0       # rank 3 is up-right of rank 0
+    hs = [w._start("y", 0, w.prv) for w in ws]
+    for w, h in zip(ws, hs):
+        w._finish("y", w.prv, h)
+    hs = [w._start("x", 0, w.prv) for w in ws]
+    for w, h in zip(ws, hs):
+        w._finish("x", w.prv, h)
+    torch.cuda.synchronize()
+    assert ws[0].prv.pops[l, g.Hx + g.Lx, g.Hy + g.Ly].item() == 7.0
+
+
+def test_wall_rank_outer_halo_untouched_by_exchange(vs):
+    """test_runtime.py:188-214."""
+    ws = _workers(vs, 8, 8, 2, (1, 2))
+    for w in ws:
+        g = w.geom
+        blk = torch.arange(37 * g.Lx * g.Ly, dtype=torch.float64, device="cuda").reshape(
+            37, g.Lx, g.Ly) + 1000.0 * (w.tile.rank + 1)
+        w.prv.pops.zero_()
+        w.prv.pops[:, g.phys_x, g.phys_y] = blk
+        w._extend_wall_halos(w.prv)
+    torch.cuda.synchronize()
+    g = ws[0].geom
+    lo = ws[0].prv.pops[:, g.phys_x, g.Hy].clone()
+    hi = ws[1].prv.pops[:, g.phys_x, g.Hy + g.Ly - 1].clone()
+    hs = [w._start("y", 0, w.prv) for w in ws]
+    for w, h in zip(ws, hs):
+        w._finish("y", w.prv, h)
+    hs = [w._start("x", 0, w.prv) for w in ws]
+    for w, h in zip(ws, hs):
+        w._finish("x", w.prv, h)
+    torch.cuda.synchronize()
+    for k in range(g.Hy):
+        assert torch.equal(ws[0].prv.pops[:, g.phys_x, k], lo)
+        assert torch.equal(ws[1].prv.pops[:, g.phys_x, g.Hy + g.Ly + k], hi)
 
 
 def test_pgm_bytes_match_reference(tmp_path):

@@ -189,10 +189,9 @@ def _run(vs, f0, steps, params, schedule, Np=1, walls=True, periodic_y=False):
         w.load_block(torch.as_tensor(f0[:, t.x0:t.x0 + t.Lx]))
         ws.append(w)
     for s in range(steps):
-        for w in ws:
-            w.step_begin(s)
-        for w in ws:
-            w.step_end(s)
+        for phase in ("step_begin", "step_mid", "step_end"):
+            for w in ws:
+                getattr(w, phase)(s)
     out = np.empty_like(f0)
     negs = []
     for w in ws:
