@@ -212,7 +212,8 @@ def gpu_arm(args, rank, world, local_rank):
     tiles = tl.decompose(Lx, Ly, world, "1d")
     tile = tiles[rank]
     fabric = tl.DistFabric() if world > 1 else tl.Fabric(1)
-    w = tl.RankWorker(tile, vs, p, fabric, schedule=args.schedule, device=dev)
+    w = tl.RankWorker(tile, vs, p, fabric, schedule=args.schedule, device=dev,
+                      exchange=args.exchange)
     macro = tl.init.rayleigh_taylor_macro(Lx, Ly, vs)
     sl = slice(tile.x0, tile.x0 + Lx_tile)
     f0 = tl.equilibrium(*[torch.as_tensor(np.ascontiguousarray(a[sl]), device=dev)
@@ -349,6 +350,7 @@ def gpu_arm(args, rank, world, local_rank):
                  else " on 1 B200 (BASELINE configs[1])")),
                 "Lx": Lx, "Ly": Ly, "tiling": "1d", "schedule": args.schedule,
                 "arith": args.arith, "tau": 0.8, "gy": -1e-5,
+                "exchange": args.exchange if world > 1 else None,
                 "l2": "no flush: 2 x %.2f GB state per GPU >> 126 MB L2" % (
                     37 * (Lx_tile + 6) * (Ly + 6) * 8 / 1e9)},
             "gflops_fp64": round(gflops, 2),
@@ -366,7 +368,8 @@ def gpu_arm(args, rank, world, local_rank):
                                   "flops_per_site": FLOP_SITE}},
             "clocks": clocks,
             "host_enqueue_ms_per_step": round(host_ms, 4),
-            "gpu_launches": args.steps * (1 if world == 1 else 4),
+            "gpu_launches": args.steps * (1 if world == 1 else
+                                          (2 if args.exchange == "p2p" else 4)),
         }
         if split:
             out["split"] = split
@@ -487,6 +490,9 @@ def main():
     ap.add_argument("--no-compare", dest="compare", action="store_false",
                     help="skip timing the other arithmetic")
     ap.add_argument("--schedule", default="overlapped", choices=["overlapped", "staged"])
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "p2p"],
+                    help="N>1 X-halo transport: NCCL ring, or NVLink peer stores fused "
+                         "into the step kernel")
     ap.add_argument("--Lx", type=int, default=TILE_LX, help="tile Lx per GPU")
     ap.add_argument("--Ly", type=int, default=TILE_LY)
     ap.add_argument("--strong", action="store_true",

@@ -50,6 +50,7 @@ typedef struct CUstream_st *tlb_stream_t; /* == cudaStream_t */
 #define TLB_ST_DEGENERATE 1u /* rho <= 0 (or NaN) in moments  kernels.py:62-66  */
 #define TLB_ST_SHIFT 2u      /* T_bar <= 0 in apply_shift     kernels.py:134-135 */
 #define TLB_ST_EQ_DOMAIN 4u  /* rho<=0 or T<=0, checked eq.   kernels.py:85-86   */
+#define TLB_ST_PEER_TIMEOUT 8u /* peer step: a neighbour did not publish in time */
 
 /* field view */
 typedef struct TlbField {
@@ -231,6 +232,29 @@ int tlb_ring_step(tlb_ring_t ring, const TlbField *prv, const TlbField *nxt,
                   const TlbParams *p, int flags, TlbStatus *status,
                   double *sbuf, double *rbuf, void *ev_bulk0, void *ev_bulk1,
                   tlb_stream_t stream);
+
+/* ---- X-halo exchange fused into the step over NVLink peer memory --------
+ * (1-D ring, one process per GPU).  The border threads of a step store their
+ * outputs both locally and into the neighbours' nxt halo columns through
+ * CUDA-IPC mapped pointers; a 1-thread kernel then publishes the step into
+ * the neighbours' mailboxes; border blocks of the next step wait for both
+ * neighbours (bounded; TLB_ST_PEER_TIMEOUT on expiry).  Replaces pack ->
+ * NCCL -> unpack of tlb_ring_step. */
+typedef struct TlbPeer *tlb_peer_t;
+/* 64-byte cudaIpcMemHandle of the allocation holding ptr, and ptr's offset */
+int tlb_ipc_handle(const void *ptr, char *out64, int64_t *offset);
+/* handles/offsets (6 each): left A, left B, left mailbox, right A, right B,
+ * right mailbox; A = the buffer that is prv at even peer steps. */
+int tlb_peer_create(int device, const char *handles, const int64_t *offsets,
+                    tlb_peer_t *out);
+int tlb_peer_destroy(tlb_peer_t peer);
+/* One step.  nxt_index: 0 if nxt is buffer A, 1 if B.  mailbox: this rank's
+ * 2 x u64 device mailbox ([0] left neighbour done, [1] right done; zeroed).
+ * peer_step: 0, 1, 2, ... (border blocks wait for mailbox >= peer_step). */
+int tlb_peer_step(tlb_peer_t peer, const TlbField *prv, const TlbField *nxt,
+                  int nxt_index, const TlbParams *p, int flags,
+                  TlbStatus *status, unsigned long long *mailbox,
+                  int64_t peer_step, tlb_stream_t stream);
 
 /* Snapshot image (io.write_pgm, io.py:13-24): min-max normalised 8-bit
  * quantisation of a (nx, ny) field with row stride ld into img (nx*ny bytes,

@@ -1130,3 +1130,6 @@ extern "C" int tlb_pgm_image(const double *v, int64_t nx, int64_t ny, int64_t ld
     k_quantize<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(v, nx, ny, ld, minmax2, img);
     return launch_check("quantize");
 }
+
+// X-halo exchange fused into the step kernel over NVLink peer memory
+#include "tlb_peer.cuh"

@@ -1,0 +1,267 @@
+// tlb_peer.cuh -- the X-halo exchange fused into the step kernel over
+// NVLink peer memory (1-D ring, one process per GPU).
+//
+// The border columns a rank computes at step s are exactly the halo its
+// neighbours read at step s+1.  So instead of pack -> NCCL -> unpack, the
+// threads that compute the 3 edge columns store their 37 outputs twice: into
+// the local nxt buffer and, through CUDA-IPC-mapped pointers, straight into
+// the neighbour's nxt buffer's halo columns (NVLink stores).  One launch per
+// step does bulk + borders + the transfer; a 1-thread signal kernel then
+// publishes "step s done" into both neighbours' mailboxes (st.release.sys).
+//
+// Ordering (both directions reduce to one condition): at step s a rank's
+// border blocks may (a) read its own halo, written by the neighbours during
+// their step s-1, and (b) overwrite the neighbours' nxt halo, which the
+// neighbours last read during their step s-1.  Border blocks therefore wait
+// until both neighbours have published step s-1 (mailbox >= s).  Bulk blocks
+// never wait.  Border blocks get the HIGHEST block indices, so by the time
+// they are scheduled the neighbours are normally done; the wait is bounded
+// (TLB_PEER_TIMEOUT_NS) and reports TLB_ST_PEER_TIMEOUT instead of hanging.
+#pragma once
+
+#define TLB_PEER_TIMEOUT_NS 5000000000ull
+
+struct TlbPeer {
+    int device = 0;
+    // neighbours' buffers A/B (A = the one that is prv at even peer steps)
+    double *left[2] = {nullptr, nullptr}, *right[2] = {nullptr, nullptr};
+    unsigned long long *left_mb = nullptr, *right_mb = nullptr;  // their mailboxes
+    void *opened[6] = {};
+};
+
+struct PeerLaunch {
+    double *rleft, *rright;        // neighbours' nxt buffers (same layout as ours)
+    unsigned long long *mb;        // our mailbox: [0] left done, [1] right done
+    long long need;                // wait until both >= need
+    int x_left0, x_right0, h;      // border bands [x_left0, +h), [x_right0, +h)
+    int Lx;
+    unsigned nbb;                  // border blocks (the last ones)
+    Rect br[2];
+    unsigned br_end[2];
+};
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+template <bool EXACT>
+__global__ void __launch_bounds__(128, 4)
+    k_peer_step(const __grid_constant__ SiteLaunch L, const __grid_constant__ PeerLaunch P) {
+    const unsigned nmain = gridDim.x - P.nbb;
+    if (blockIdx.x < nmain) {
+        // wall frames first, then the branch-free interior: exactly k_site
+        if (blockIdx.x < L.nfb) {
+            const unsigned total = L.fr_end[3];
+            const unsigned i = blockIdx.x * blockDim.x + threadIdx.x;
+            const bool active = i < total;
+            const unsigned ii = active ? i : total - 1;
+            const int r = ii < L.fr_end[0] ? 0 : ii < L.fr_end[1] ? 1 : ii < L.fr_end[2] ? 2 : 3;
+            const unsigned loc = ii - (r ? L.fr_end[r - 1] : 0u);
+            const Rect &R = L.fr[r];
+            site_body<K_FUSED, EXACT, 4, false, true>(L, R.x0 + (int)(loc / R.ny),
+                                                      R.y0 + (int)(loc % R.ny), active);
+        } else {
+            const unsigned i = (blockIdx.x - L.nfb) * blockDim.x + threadIdx.x;
+            const bool active = i < L.in.n;
+            const unsigned ii = active ? i : L.in.n - 1;
+            site_body<K_FUSED, EXACT, 4, false, false>(L, L.in.x0 + (int)(ii / L.in.ny),
+                                                       L.in.y0 + (int)(ii % L.in.ny), active);
+        }
+        return;
+    }
+    // ---- border blocks: wait for both neighbours' step s-1 ----
+    __shared__ int timed_out;
+    if (threadIdx.x == 0) {
+        timed_out = 0;
+        const unsigned long long t0 = globaltimer();
+        while (ld_acquire_sys(P.mb) < (unsigned long long)P.need ||
+               ld_acquire_sys(P.mb + 1) < (unsigned long long)P.need) {
+            if (globaltimer() - t0 > TLB_PEER_TIMEOUT_NS) {
+                timed_out = 1;
+                break;
+            }
+            __nanosleep(256);
+        }
+    }
+    __syncthreads();
+    const unsigned total = P.br_end[1];
+    const unsigned i = (blockIdx.x - nmain) * blockDim.x + threadIdx.x;
+    const bool active = i < total && !timed_out;
+    const unsigned ii = i < total ? i : total - 1;
+    const int r = ii < P.br_end[0] ? 0 : 1;
+    const unsigned loc = ii - (r ? P.br_end[0] : 0u);
+    const Rect &R = P.br[r];
+    const int x = R.x0 + (int)(loc / R.ny), y = R.y0 + (int)(loc % R.ny);
+    double f[Q];
+    const bool implicit = (L.flags & (TLB_F_WRAP_Y | TLB_F_CLAMP_Y)) != 0;
+    load_all(f, L.src, x, y, true, implicit, L.flags);
+    unsigned bits = 0;
+    {
+        const bool bot = y >= L.bot_lo && y < L.bot_hi;
+        const bool top = y >= L.top_lo && y < L.top_hi;
+        if (bot || top) {
+            const double Tw = bot ? L.P.Tbot : L.P.Ttop;
+            RegF rf{f};
+            bits |= EXACT ? bc_exact<4>(rf, Tw) : bc_fast<4>(rf, Tw);
+        }
+        RegF rf{f};
+        bits |= EXACT ? collide_exact<4>(rf, L.P) : collide_fast<4>(rf, L.P);
+    }
+    if (active) {
+        report(L.status, bits, x, y, L.step);
+        store_all(f, L.dst, x, y);
+        // the neighbour's halo: our left band -> left neighbour's right halo
+        // (column + Lx), our right band -> right neighbour's left halo (- Lx)
+        const bool left_band = x < P.x_left0 + P.h;
+        double *rb = left_band ? P.rleft : P.rright;
+        const int rx = left_band ? x + P.Lx : x - P.Lx;
+        double *q = rb + (long long)rx * L.dst.sx + (long long)y * L.dst.sy;
+#pragma unroll
+        for (int l = 0; l < Q; ++l) q[(long long)l * L.dst.sl] = f[l];
+        __threadfence_system();
+    }
+    if (timed_out && threadIdx.x == 0) report(L.status, TLB_ST_PEER_TIMEOUT, x, y, L.step);
+    if (L.flags & TLB_F_COUNT_NEG) count_neg(L.status, f, active);
+}
+
+// publish "step done" (value = peer step + 1) into both neighbours' mailboxes
+__global__ void k_peer_signal(unsigned long long *left_mb, unsigned long long *right_mb,
+                              unsigned long long value) {
+    __threadfence_system();
+    // we are our left neighbour's RIGHT neighbour and vice versa
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(left_mb + 1), "l"(value) : "memory");
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(right_mb), "l"(value) : "memory");
+}
+
+extern "C" {
+
+int tlb_ipc_handle(const void *ptr, char *out64, int64_t *offset) {
+    // the IPC handle names the whole allocation: export its base + our offset
+    using GetRange = int (*)(unsigned long long *, size_t *, unsigned long long);
+    static GetRange range = nullptr;
+    if (!range) {
+        void *h = dlopen("libcuda.so.1", RTLD_NOW | RTLD_NOLOAD);
+        if (!h) h = dlopen("libcuda.so.1", RTLD_NOW);
+        if (h) range = reinterpret_cast<GetRange>(dlsym(h, "cuMemGetAddressRange_v2"));
+        if (!range) return fail(TLB_ERR_UNSUPPORTED, "cuMemGetAddressRange unavailable");
+    }
+    unsigned long long base = 0;
+    size_t size = 0;
+    if (range(&base, &size, (unsigned long long)ptr) != 0)
+        return fail(TLB_ERR_CUDA, "cuMemGetAddressRange failed");
+    cudaIpcMemHandle_t hd;
+    TLB_CUDA_CHECK(cudaIpcGetMemHandle(&hd, (void *)base));
+    memcpy(out64, &hd, sizeof hd);
+    *offset = (int64_t)((unsigned long long)ptr - base);
+    return TLB_OK;
+}
+
+int tlb_peer_create(int device, const char *handles, const int64_t *offsets, tlb_peer_t *out) {
+    TLB_CUDA_CHECK(cudaSetDevice(device));
+    TlbPeer *p = new TlbPeer();
+    p->device = device;
+    void *ptrs[6];
+    for (int k = 0; k < 6; ++k) {
+        cudaIpcMemHandle_t hd;
+        memcpy(&hd, handles + 64 * k, sizeof hd);
+        // a neighbour may appear twice (Np = 2): open each distinct handle once
+        int same = -1;
+        for (int j = 0; j < k; ++j)
+            if (!memcmp(handles + 64 * j, handles + 64 * k, sizeof hd)) same = j;
+        if (same >= 0) {
+            ptrs[k] = (char *)ptrs[same] - offsets[same];
+        } else {
+            cudaError_t e = cudaIpcOpenMemHandle(&ptrs[k], hd, cudaIpcMemLazyEnablePeerAccess);
+            if (e != cudaSuccess) {
+                for (int j = 0; j < k; ++j)
+                    if (p->opened[j]) cudaIpcCloseMemHandle(p->opened[j]);
+                delete p;
+                return fail(TLB_ERR_CUDA, "cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
+            }
+            p->opened[k] = ptrs[k];
+        }
+        ptrs[k] = (char *)ptrs[k] + offsets[k];
+    }
+    p->left[0] = (double *)ptrs[0];
+    p->left[1] = (double *)ptrs[1];
+    p->left_mb = (unsigned long long *)ptrs[2];
+    p->right[0] = (double *)ptrs[3];
+    p->right[1] = (double *)ptrs[4];
+    p->right_mb = (unsigned long long *)ptrs[5];
+    *out = p;
+    return TLB_OK;
+}
+
+int tlb_peer_destroy(tlb_peer_t p) {
+    if (!p) return TLB_OK;
+    cudaSetDevice(p->device);
+    cudaDeviceSynchronize();
+    for (int k = 0; k < 6; ++k)
+        if (p->opened[k]) cudaIpcCloseMemHandle(p->opened[k]);
+    delete p;
+    return TLB_OK;
+}
+
+int tlb_peer_step(tlb_peer_t pr, const TlbField *prv, const TlbField *nxt, int parity,
+                  const TlbParams *p, int flags, TlbStatus *status, unsigned long long *mailbox,
+                  int64_t peer_step, tlb_stream_t stream) {
+    int e;
+    if ((e = check_stencil())) return e;
+    if ((e = check_params(p))) return e;
+    if (p->order != 4) return fail(TLB_ERR_UNSUPPORTED, "peer step: order 4 only");
+    if (flags & (TLB_F_WRAP_X)) return fail(TLB_ERR_CONTRACT, "peer step: X halos are remote");
+    const int h = TLB_WALL_ROWS;
+    if (prv->Lx < 2 * h + 1) return fail(TLB_ERR_UNSUPPORTED, "peer step: tile narrower than 7");
+    cudaStream_t s = (cudaStream_t)stream;
+    SiteLaunch L;
+    memset(&L, 0, sizeof L);
+    L.src = mkfld(prv);
+    L.dst = mkfld(nxt);
+    L.P = mkphys(p);
+    L.status = status;
+    L.flags = flags;
+    L.step = -1;
+    wall_rows(L, prv, flags);
+    TlbRegion bulk = {prv->Hx + h, prv->Hx + prv->Lx - h, prv->Hy, prv->Hy + prv->Ly};
+    split_region(L, bulk, prv, flags);
+    for (int l = 0; l < Q; ++l) {
+        L.soffb[l] = 8 * ((long long)l * L.src.sl - ((long long)CX(l) * L.src.sx +
+                                                      (long long)CY(l) * L.src.sy));
+        L.doffb[l] = 8 * (long long)l * L.dst.sl;
+    }
+    L.nfb = (L.fr_end[3] + 127) / 128;
+    PeerLaunch P;
+    memset(&P, 0, sizeof P);
+    P.rleft = pr->left[parity];
+    P.rright = pr->right[parity];
+    P.mb = mailbox;
+    P.need = peer_step;
+    P.h = h;
+    P.Lx = prv->Lx;
+    P.x_left0 = prv->Hx;
+    P.x_right0 = prv->Hx + prv->Lx - h;
+    P.br[0] = mkrect(prv->Hx, prv->Hx + h, prv->Hy, prv->Hy + prv->Ly);
+    P.br[1] = mkrect(prv->Hx + prv->Lx - h, prv->Hx + prv->Lx, prv->Hy, prv->Hy + prv->Ly);
+    P.br_end[0] = P.br[0].n;
+    P.br_end[1] = P.br[0].n + P.br[1].n;
+    P.nbb = (P.br_end[1] + 127) / 128;
+    const unsigned nb = L.nfb + (L.in.n + 127) / 128 + P.nbb;
+    if (p->arith == TLB_ARITH_EXACT)
+        k_peer_step<true><<<nb, 128, 0, s>>>(L, P);
+    else
+        k_peer_step<false><<<nb, 128, 0, s>>>(L, P);
+    if ((e = launch_check("peer step"))) return e;
+    k_peer_signal<<<1, 1, 0, s>>>(pr->left_mb, pr->right_mb,
+                                  (unsigned long long)(peer_step + 1));
+    return launch_check("peer signal");
+}
+
+}  // extern "C"

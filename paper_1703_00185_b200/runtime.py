@@ -335,10 +335,12 @@ class RankWorker:
 
     def __init__(self, tile, vs, params, fabric=None, schedule="staged", walls=True,
                  layout="soa", halo=DEFAULT_HALO, debug_poison=False, device=None,
-                 periodic_y=False):
+                 periodic_y=False, exchange="nccl"):
         torch = _lib.torch_cuda()
         if schedule not in ("staged", "overlapped"):
             raise ConfigurationError(f"unknown schedule {schedule!r}")
+        if exchange not in ("nccl", "p2p"):
+            raise ConfigurationError(f"unknown exchange {exchange!r} (nccl|p2p)")
         self.tile = tile
         self.vs = vs
         self.params = params
@@ -387,6 +389,10 @@ class RankWorker:
                     ctypes.c_void_p(self.ybuf4.data_ptr())), "ring neighbours")
             self._status_ring = torch.zeros((self._RING, _lib.STATUS_BYTES),
                                             dtype=torch.uint8, device=self.device)
+            self._peer = None
+            if (exchange == "p2p" and self._ring is not None and not self.y_exchange
+                    and not self.x_self and schedule == "overlapped"):
+                self._setup_peer(fabric)
             # order the allocations' zero-fills before any work on our stream
             self.stream.wait_stream(torch.cuda.current_stream(self.device))
         self.plans = face_plans(vs, halo)
@@ -395,6 +401,36 @@ class RankWorker:
         self._retained = []
         self._metrics = []
         self.snapshots = []
+        self._primed = False
+
+    def _setup_peer(self, fabric):
+        """Map the ring neighbours' field buffers and mailboxes (CUDA IPC over
+        NVLink) for the fused peer-memory step (csrc/tlb_peer.cuh)."""
+        import ctypes
+        torch = _lib.torch_cuda()
+        lib = _lib.load()
+        self.mailbox = torch.zeros(2, dtype=torch.int64, device=self.device)
+        torch.cuda.synchronize(self.device)
+        mine = []
+        for t in (self.prv.data, self.nxt.data, self.mailbox):
+            h = ctypes.create_string_buffer(64)
+            off = ctypes.c_int64(0)
+            _lib.check(lib.tlb_ipc_handle(t.data_ptr(), h, ctypes.byref(off)), "ipc handle")
+            mine.append((bytes(h.raw), int(off.value)))
+        allinfo = [None] * fabric.Np
+        fabric.dist.all_gather_object(allinfo, mine, group=fabric.group)
+        nb = self.tile.neighbors
+        order = allinfo[nb["left"]] + allinfo[nb["right"]]
+        handles = b"".join(h for h, _ in order)
+        offs = (ctypes.c_int64 * 6)(*[o for _, o in order])
+        hp = ctypes.c_void_p()
+        _lib.check(lib.tlb_peer_create(self.device.index, handles, offs, ctypes.byref(hp)),
+                   "peer create")
+        self._peer = hp
+        self._bufA = self.prv.data.data_ptr()
+        self._peer_step = 0
+        self._primed = False
+        fabric.dist.barrier(group=fabric.group)
 
     # -- helpers -------------------------------------------------------------
     @property
@@ -612,6 +648,24 @@ class RankWorker:
             return
         flags = self._flags()
         self._flags_now = flags
+        if self._peer is not None:
+            if not self._primed:
+                # fill prv's halos once through NCCL; afterwards every step's
+                # border threads write the neighbours' halos directly
+                self._check(lib.tlb_ring_exchange(
+                    self._ring, field_desc(self.prv), self._ymode(), self.sbuf2.data_ptr(),
+                    self.rbuf2.data_ptr(), self._sp()), "ring exchange")
+                self._primed = True
+            nxt_index = 0 if self.nxt.data.data_ptr() == self._bufA else 1
+            ev[1].record(self.stream)
+            self._check(lib.tlb_peer_step(
+                self._peer, field_desc(self.prv), field_desc(self.nxt), nxt_index,
+                self.tparams, flags, st, self.mailbox.data_ptr(), self._peer_step,
+                self._sp()), "peer step")
+            self._peer_step += 1
+            ev[2].record(self.stream)
+            self._bulk_timed = True
+            return
         if self._ring is not None:
             ev[1].record(self.stream)
             ev[2].record(self.stream)
@@ -682,7 +736,8 @@ class RankWorker:
             self._check(lib.tlb_collide(field_desc(self.nxt), field_desc(self.nxt), full,
                                         self.tparams, _lib.F_COUNT_NEG, st, self._sp()),
                         "collide")
-        elif self._ring is None and not (self.x_self and not self.y_exchange):
+        elif (self._ring is None and self._peer is None
+              and not (self.x_self and not self.y_exchange)):
             # halos in -> frame bands on the side stream, concurrent with bulk
             cs = self.comm_stream
             if self._hx is not None:
@@ -697,6 +752,13 @@ class RankWorker:
     # -- results -------------------------------------------------------------
     def synchronize(self):
         self.stream.synchronize()
+
+    def close(self):
+        """Release the peer mappings (after every rank finished its steps)."""
+        if getattr(self, "_peer", None) is not None:
+            self.synchronize()
+            _lib.load().tlb_peer_destroy(self._peer)
+            self._peer = None
 
     def collect(self, raise_errors=True):
         """Materialise pending per-step metrics (one host sync) and raise the
@@ -728,6 +790,10 @@ class RankWorker:
             self._status_ring.zero_()
         if err is not None and raise_errors:
             step, s = err
+            if s.flags & _lib.ST_PEER_TIMEOUT:
+                raise DeadlockError(f"rank {self.tile.rank} step {step}: a ring neighbour did "
+                                    "not publish its step (peer-memory exchange)",
+                                    rank=self.tile.rank)
             if s.flags & _lib.ST_EQ_DOMAIN:
                 raise DomainError(f"rank {self.tile.rank} step {step}: "
                                   "equilibrium requires rho > 0 and T > 0")
@@ -757,6 +823,7 @@ class RankWorker:
     def load_block(self, block):
         """prv[phys] = block (sim.py:74-75); block is (Q, Lx, Ly)."""
         torch = _lib.torch_cuda()
+        self._primed = False
         g = self.geom
         self.stream.wait_stream(torch.cuda.current_stream(self.device))
         with torch.cuda.stream(self.stream):

@@ -48,6 +48,7 @@ class SimConfig:
     recv_timeout: float = 60.0
     devices: "tuple | None" = None
     output: str = "host"
+    exchange: str = "nccl"   # one process per GPU: "nccl" ring or "p2p" (NVLink peer stores)
 
     def __post_init__(self):
         if self.schedule not in ("staged", "overlapped"):
@@ -120,7 +121,7 @@ def run(cfg: SimConfig, f0=None) -> RunResult:
             w = RankWorker(tile, vs, cfg.params, fabric, schedule=cfg.schedule,
                            walls=cfg.walls, layout=cfg.layout, halo=cfg.halo,
                            debug_poison=cfg.debug_poison, device=dev,
-                           periodic_y=cfg.periodic_y)
+                           periodic_y=cfg.periodic_y, exchange=cfg.exchange)
             sl = (slice(tile.x0, tile.x0 + tile.Lx), slice(tile.y0, tile.y0 + tile.Ly))
             if macro0 is not None:
                 ts = [torch.as_tensor(np.ascontiguousarray(a[sl], dtype=np.float64),
@@ -180,6 +181,10 @@ def run(cfg: SimConfig, f0=None) -> RunResult:
         mine = blocks[0][1]
         gathered = [torch.empty_like(mine) for _ in range(cfg.Np)] if rank == 0 else None
         dist.gather(mine, gathered, dst=0)
+        dist.barrier()
+        for w in workers:
+            w.close()
+        fabric.close()
         if rank != 0:
             mlups = cfg.Lx * cfg.Ly * cfg.steps / (wall * 1e6) if cfg.steps else 0.0
             return RunResult(None, None, metrics, mlups, wall, [])

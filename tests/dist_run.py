@@ -39,15 +39,23 @@ def main():
         want, neg = O.run(f0, steps, O.params6(p.tau, p.gx, p.gy, p.dt, p.Twall_top,
                                                  p.Twall_bot))
     tilings = ["1d", (1, world)] + ([(2, world // 2)] if world >= 4 else [])
+    cases = [(t, sch, "nccl") for t in tilings for sch in ("overlapped", "staged")]
+    cases.append(("1d", "overlapped", "p2p"))      # NVLink peer-store exchange
     ok = True
-    for tiling in tilings:
-        for schedule in ("overlapped", "staged"):
+    for tiling, schedule, exchange in cases:
+        for arith in (("exact", "fast") if exchange == "p2p" else ("exact",)):
+            pp = tl.PhysicsParams(tau=p.tau, gx=p.gx, gy=p.gy, Twall_top=p.Twall_top,
+                                  Twall_bot=p.Twall_bot, arith=arith)
             res = tl.run(tl.SimConfig(Lx=Lx, Ly=Ly, Np=world, tiling=tiling, steps=steps,
-                                      params=p, init="rayleigh-taylor", schedule=schedule))
+                                      params=pp, init="rayleigh-taylor", schedule=schedule,
+                                      exchange=exchange))
             if rank == 0:
-                same = np.array_equal(res.populations, want)
-                print(f"tiling={tiling} schedule={schedule} world={world} bitwise={same} "
-                      f"mlups={res.mlups:.1f}", flush=True)
+                if arith == "exact":
+                    same = np.array_equal(res.populations, want)
+                else:
+                    same = bool(np.max(np.abs(res.populations - want) / np.abs(want)) < 1e-12)
+                print(f"tiling={tiling} schedule={schedule} exchange={exchange} arith={arith} "
+                      f"world={world} ok={same} mlups={res.mlups:.1f}", flush=True)
                 ok &= same
             assert len(res.metrics) == steps
     dist.barrier()
