@@ -14,9 +14,12 @@
 // their step s-1, and (b) overwrite the neighbours' nxt halo, which the
 // neighbours last read during their step s-1.  Border blocks therefore wait
 // until both neighbours have published step s-1 (mailbox >= s).  Bulk blocks
-// never wait.  Border blocks get the HIGHEST block indices, so by the time
-// they are scheduled the neighbours are normally done; the wait is bounded
-// (TLB_PEER_TIMEOUT_NS) and reports TLB_ST_PEER_TIMEOUT instead of hanging.
+// never wait.  Border blocks get the LOWEST block indices: in lock step the
+// neighbours publish within microseconds, and a border block that waits
+// holds one CTA slot while the bulk fills the rest of the GPU (placing them
+// last instead leaves their latency as a tail: measured slower).  The wait
+// is bounded (TLB_PEER_TIMEOUT_NS) and reports TLB_ST_PEER_TIMEOUT instead of
+// hanging.
 #pragma once
 
 #define TLB_PEER_TIMEOUT_NS 5000000000ull
@@ -55,12 +58,13 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 template <bool EXACT>
 __global__ void __launch_bounds__(128, 4)
     k_peer_step(const __grid_constant__ SiteLaunch L, const __grid_constant__ PeerLaunch P) {
-    const unsigned nmain = gridDim.x - P.nbb;
-    if (blockIdx.x < nmain) {
-        // wall frames first, then the branch-free interior: exactly k_site
-        if (blockIdx.x < L.nfb) {
+    // border blocks first (they may wait briefly for the neighbours while the
+    // bulk fills the rest of the GPU), then wall frames, then the interior
+    if (blockIdx.x >= P.nbb) {
+        const unsigned b = blockIdx.x - P.nbb;
+        if (b < L.nfb) {
             const unsigned total = L.fr_end[3];
-            const unsigned i = blockIdx.x * blockDim.x + threadIdx.x;
+            const unsigned i = b * blockDim.x + threadIdx.x;
             const bool active = i < total;
             const unsigned ii = active ? i : total - 1;
             const int r = ii < L.fr_end[0] ? 0 : ii < L.fr_end[1] ? 1 : ii < L.fr_end[2] ? 2 : 3;
@@ -69,7 +73,7 @@ __global__ void __launch_bounds__(128, 4)
             site_body<K_FUSED, EXACT, 4, false, true>(L, R.x0 + (int)(loc / R.ny),
                                                       R.y0 + (int)(loc % R.ny), active);
         } else {
-            const unsigned i = (blockIdx.x - L.nfb) * blockDim.x + threadIdx.x;
+            const unsigned i = (b - L.nfb) * blockDim.x + threadIdx.x;
             const bool active = i < L.in.n;
             const unsigned ii = active ? i : L.in.n - 1;
             site_body<K_FUSED, EXACT, 4, false, false>(L, L.in.x0 + (int)(ii / L.in.ny),
@@ -93,7 +97,7 @@ __global__ void __launch_bounds__(128, 4)
     }
     __syncthreads();
     const unsigned total = P.br_end[1];
-    const unsigned i = (blockIdx.x - nmain) * blockDim.x + threadIdx.x;
+    const unsigned i = blockIdx.x * blockDim.x + threadIdx.x;
     const bool active = i < total && !timed_out;
     const unsigned ii = i < total ? i : total - 1;
     const int r = ii < P.br_end[0] ? 0 : 1;

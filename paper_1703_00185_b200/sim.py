@@ -49,6 +49,7 @@ class SimConfig:
     devices: "tuple | None" = None
     output: str = "host"
     exchange: str = "nccl"   # one process per GPU: "nccl" ring or "p2p" (NVLink peer stores)
+    timing: str = "sampled"  # per-step device timers: "sampled" (1 in 32), "every", "off"
 
     def __post_init__(self):
         if self.schedule not in ("staged", "overlapped"):
@@ -121,7 +122,8 @@ def run(cfg: SimConfig, f0=None) -> RunResult:
             w = RankWorker(tile, vs, cfg.params, fabric, schedule=cfg.schedule,
                            walls=cfg.walls, layout=cfg.layout, halo=cfg.halo,
                            debug_poison=cfg.debug_poison, device=dev,
-                           periodic_y=cfg.periodic_y, exchange=cfg.exchange)
+                           periodic_y=cfg.periodic_y, exchange=cfg.exchange,
+                           timing=cfg.timing)
             sl = (slice(tile.x0, tile.x0 + tile.Lx), slice(tile.y0, tile.y0 + tile.Ly))
             if macro0 is not None:
                 ts = [torch.as_tensor(np.ascontiguousarray(a[sl], dtype=np.float64),
