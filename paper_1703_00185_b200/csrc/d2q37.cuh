@@ -160,9 +160,15 @@ __device__ __forceinline__ double pdot_exact(double vx, double vy) {
 }
 
 // Site-level quantities of equilibrium() (kernels.py:87-91, 100-121).
+// Power-of-two identities keep these bitwise equal to the reference while
+// saving operations: RN(2^k x) = 2^k RN(x) and fma(2^k, a, b) = RN(b + 2^k a)
+// (exact products; no subnormal intermediates occur for lattice states).
+// Hence 6*theta = 2*RN(3*theta), RN(6 theta q) = 2 RN(3 theta q),
+// RN(RN(6p) p) = 2 RN(RN(3p) p), (8 theta) s = 8 RN(theta s), and the
+// reference's (theta*theta*4)*q = 4 RN(theta theta q).
 struct EqSite {
     double rho, vx, vy, theta, s;
-    double s2t, s4t, t3, t6, t3t, tt4, c3x;
+    double s2t, s4t, t3, t3t, tt, c3x;
 };
 
 __device__ __forceinline__ EqSite eq_site_exact(double rho, double ux, double uy,
@@ -174,21 +180,20 @@ __device__ __forceinline__ EqSite eq_site_exact(double rho, double ux, double uy
     e.theta = dsub(div_const2(T, C.cs2, C.rcs2), 1.0);
     e.s = dadd(dmul(e.vx, e.vx), dmul(e.vy, e.vy));
     const double th = e.theta;
-    e.s2t = dadd(e.s, dmul(2.0, th));          // s + D*theta
-    e.s4t = dadd(e.s, dmul(4.0, th));          // s + (D+2)*theta
-    e.t3 = dmul(3.0, th);                      // 3.0*theta
-    e.t6 = dmul(6.0, th);                      // 6.0*theta
+    e.s2t = dfma(2.0, th, e.s);                // s + D*theta
+    e.s4t = dfma(4.0, th, e.s);                // s + (D+2)*theta
+    e.t3 = dmul(3.0, th);                      // 3.0*theta (6.0*theta == 2*t3)
     e.t3t = dmul(e.t3, th);                    // 3.0*theta*theta
-    e.tt4 = dmul(dmul(th, th), 4.0);           // theta*theta*(D+2)
-    const double t8 = dmul(8.0, th);           // (2D+4)*theta == D(D+2)*theta
-    const double inner3 = dadd(dadd(dmul(e.s, e.s), dmul(t8, e.s)), dmul(t8, th));
+    e.tt = dmul(th, th);                       // theta*theta
+    // ((s*s) + ((8 theta) s)) + ((8 theta) theta)
+    const double inner3 = dfma(8.0, e.tt, dfma(8.0, dmul(th, e.s), dmul(e.s, e.s)));
     e.c3x = dmul(3.0, inner3);
     return e;
 }
 
 // Per-shell sub-expressions (depend on q only).
 struct EqShell {
-    double tq, t3q, t6q, t3tqq, qs, tt4q, wr;
+    double tq, t3q, t3tqq, qs, ttq, wr;
 };
 
 template <int sh>
@@ -196,16 +201,16 @@ __device__ __forceinline__ EqShell eq_shell_exact(const EqSite &e) {
     const double q = C.qsh[sh];
     EqShell z;
     z.tq = dmul(e.theta, q);
-    z.t3q = dmul(e.t3, q);
-    z.t6q = dmul(e.t6, q);
+    z.t3q = dmul(e.t3, q);                     // (6 theta) q == 2 t3q
     z.t3tqq = dmul(dmul(e.t3t, q), q);
     z.qs = dmul(q, e.s);
-    z.tt4q = dmul(e.tt4, q);
+    z.ttq = dmul(e.tt, q);                     // (theta theta 4) q == 4 ttq
     z.wr = dmul(C.wsh[sh], e.rho);             // w*rho
     return z;
 }
 
-// Equilibrium pair (feq for +c and -c) with the reference rounding.
+// Equilibrium pair (feq for +c and -c) with the reference rounding
+// (kernels.py:98-124).
 template <int ORDER>
 __device__ __forceinline__ void eq_pair_exact(const EqSite &e, const EqShell &z,
                                               double p, double &fp, double &fm) {
@@ -215,17 +220,19 @@ __device__ __forceinline__ void eq_pair_exact(const EqSite &e, const EqShell &z,
     double bm = dfma(0.5, c2, dsub(1.0, p));
     if constexpr (ORDER >= 3) {
         const double ppp = dmul(pp, p);
-        const double c3 = dsub(dadd(ppp, dmul(z.t3q, p)), dmul(dmul(3.0, p), e.s4t));
+        const double w3 = dmul(z.t3q, p);                   // ((3 theta) q) p
+        const double p3 = dmul(3.0, p);                      // 3.0*p
+        const double c3 = dsub(dadd(ppp, w3), dmul(p3, e.s4t));
         const double d6 = div_const1(c3, 6.0, C.r6);
         bp = dadd(bp, d6);
         bm = dsub(bm, d6);
         if constexpr (ORDER >= 4) {
             const double pppp = dmul(ppp, p);
-            const double B = dmul(dmul(z.t6q, p), p);
-            const double sum1 = dadd(dadd(pppp, B), z.t3tqq);
-            const double in6 = dadd(dadd(dmul(dmul(e.s, p), p),
-                                         dmul(e.theta, dadd(dmul(dmul(6.0, p), p), z.qs))),
-                                    z.tt4q);
+            // (((6 theta) q) p) p == 2 RN(w3 p);  ((6 p) p) == 2 RN(p3 p)
+            const double sum1 = dadd(dfma(2.0, dmul(w3, p), pppp), z.t3tqq);
+            const double in6 = dfma(4.0, z.ttq,
+                                    dadd(dmul(dmul(e.s, p), p),
+                                         dmul(e.theta, dfma(2.0, dmul(p3, p), z.qs))));
             const double c4 = dadd(dsub(sum1, dmul(6.0, in6)), e.c3x);
             const double d24 = div_const1(c4, 24.0, C.r24);
             bp = dadd(bp, d24);

@@ -215,9 +215,10 @@ __device__ __forceinline__ void load_inplace(double (&f)[Q], const Fld &s, int x
 // Interior loads: one site pointer plus the launch's precomputed byte
 // offsets of the 37 (shifted) population sources -- no branches, all 37
 // loads issued back to back, two integer adds each.
-// STREAM: L1::no_allocate loads (and streaming stores, see RegStoreF) --
-// measured +2 % for the exact collide, -5 % for fast and propagate
-// (profiles/r01_summary.md), so only the exact fused path uses them.
+// STREAM: L1::no_allocate loads (and streaming stores, see RegStoreF).
+// Measured -3 % (exact, after the power-of-two arithmetic savings) and -5 %
+// (fast, propagate) on B200 (profiles/r01_summary.md): kept as an option,
+// not used.
 template <bool STREAM>
 __device__ __forceinline__ void load_plain(double (&f)[Q], const SiteLaunch &L, int x, int y) {
     const char *sp = reinterpret_cast<const char *>(
@@ -290,7 +291,7 @@ __device__ __forceinline__ void site_body(const SiteLaunch &L, int x, int y, boo
         const bool implicit = (L.flags & (TLB_F_WRAP_X | TLB_F_WRAP_Y | TLB_F_CLAMP_Y)) != 0;
         load_all(f, L.src, x, y, gather, implicit, L.flags);
     } else {
-        load_plain<EXACT && KIND == K_FUSED>(f, L, x, y);
+        load_plain<false>(f, L, x, y);
     }
     unsigned bits = 0;
     if (EDGE && (KIND == K_BC || KIND == K_FUSED)) {
@@ -317,7 +318,7 @@ __device__ __forceinline__ void site_body(const SiteLaunch &L, int x, int y, boo
     if constexpr (!EDGE && !INPLACE && (KIND == K_COLLIDE || KIND == K_FUSED)) {
         char *dp = reinterpret_cast<char *>(L.dst.base + (long long)x * L.dst.sx +
                                             (long long)y * L.dst.sy);
-        RegStoreF<EXACT && KIND == K_FUSED> sf{f, dp, L.doffb, active, 0u};
+        RegStoreF<false> sf{f, dp, L.doffb, active, 0u};
         bits |= EXACT ? collide_exact<ORDER>(sf, L.P) : collide_fast<ORDER>(sf, L.P);
         if (active) report(L.status, bits, x, y, L.step);
         if (L.flags & TLB_F_COUNT_NEG) count_neg_n(L.status, sf.neg);
