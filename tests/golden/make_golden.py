@@ -182,6 +182,31 @@ def main():
     np.savez(os.path.join(HERE, "io.npz"), T=T, pgm=np.frombuffer(pgm, dtype=np.uint8),
              macro_small=r["rt_f20_macro"][:, :4, :3], csv=np.array(csv_txt))
 
+    # -------------------------------------------------------- planner --
+    from thermolb import planner as P
+    rng = np.random.default_rng(0)
+    rows, ins = [], []
+    tab = P.BandwidthTable([1e3, 1e5, 1e7], [2e9, 3e10, 6e11])
+    for k in range(40):
+        Lx = int(rng.integers(64, 4000)); Ly = Lx if k % 4 == 0 else int(rng.integers(64, 4000))
+        Np = int(rng.integers(1, 64))
+        Bx = float(rng.uniform(1e8, 1e12)); By = float(rng.uniform(1e8, 1e12))
+        beta = float(rng.uniform(1e-10, 1e-7)); S = float(rng.uniform(8, 400))
+        use_tab = k % 3 == 0
+        inp = P.CostModelInput(Lx, Ly, Np, tab if use_tab else Bx, tab if use_tab else By,
+                               beta, S)
+        real, best = P.optimal_grid(inp)
+        vals = [P.predict_1d(inp).T_total, P.predict_2d(inp).T_total,
+                P.predict_2d(inp, grid=best).T_total, P.predict_1d_overlap(inp).T_total,
+                P.predict_1d_overlap(inp).scale_violation,
+                P.predict_2d_overlap(inp).T_total if Lx == Ly else np.nan,
+                P.comm_time_2d(inp, *best), real[0], real[1], best[0], best[1],
+                P.surface_over_volume(Np, 2), P.brent_bound(beta, Lx * Ly, Np)]
+        ins.append([Lx, Ly, Np, Bx, By, beta, S, use_tab])
+        rows.append(vals)
+    np.savez(os.path.join(HERE, "planner.npz"), inputs=np.array(ins, dtype=np.float64),
+             outputs=np.array(rows, dtype=np.float64), tab_sizes=tab.sizes, tab_bw=tab.bandwidths)
+
     # ---------------------------------------------------- fingerprints --
     fp = {"w": sha16(vs.w), "cs2": float.hex(float(vs.cs2))}
     cfg = SimConfig(Lx=256, Ly=128, model="D2Q37", Np=1, tiling="1d",

@@ -184,3 +184,36 @@ def test_load_config(tmp_path):
         tio.load_config(p)
     with pytest.raises(tl.ConfigurationError):
         tio.load_config(tmp_path / "missing.yaml")
+
+
+# --------------------------------------------------------------- planner --
+
+def test_planner_matches_reference():
+    from paper_1703_00185_b200 import planner as P
+    g = golden("planner.npz")
+    tab = P.BandwidthTable(g["tab_sizes"], g["tab_bw"])
+    for row, want in zip(g["inputs"], g["outputs"]):
+        Lx, Ly, Np, Bx, By, beta, S, use_tab = row
+        Lx, Ly, Np = int(Lx), int(Ly), int(Np)
+        inp = P.CostModelInput(Lx, Ly, Np, tab if use_tab else Bx, tab if use_tab else By,
+                               beta, S)
+        real, best = P.optimal_grid(inp)
+        got = [P.predict_1d(inp).T_total, P.predict_2d(inp).T_total,
+               P.predict_2d(inp, grid=best).T_total, P.predict_1d_overlap(inp).T_total,
+               P.predict_1d_overlap(inp).scale_violation,
+               P.predict_2d_overlap(inp).T_total if Lx == Ly else np.nan,
+               P.comm_time_2d(inp, *best), real[0], real[1], best[0], best[1],
+               P.surface_over_volume(Np, 2), P.brent_bound(beta, Lx * Ly, Np)]
+        assert np.allclose(got, want, rtol=1e-12, atol=0, equal_nan=True), (row, got, want)
+
+
+def test_planner_limits():
+    from paper_1703_00185_b200 import planner as P
+    inp = P.CostModelInput(4096, 4096, 8, Bx=1e30, By=1e30, beta=1e-8)
+    assert abs(P.predict_1d_overlap(inp).scale_violation - 1.0) < 1e-9
+    with pytest.raises(tl.UnsupportedCaseError):
+        P.predict_2d_overlap(P.CostModelInput(100, 200, 4, 1e9, 1e9, 1e-8))
+    with pytest.raises(tl.ContractViolation):
+        P.CostModelInput(0, 10, 1, 1e9, 1e9, 1e-8)
+    rows = P.scaling_curve(P.CostModelInput(512, 512, 1, 1e11, 1e11, 1e-10), [1, 2, 4])
+    assert {r[1] for r in rows} == {"1d", "2d", "1d_overlap", "2d_overlap"}
