@@ -108,6 +108,16 @@ int tlb_device_count(void);
  * not the D2Q37 ordering or w is not constant per speed shell. */
 int tlb_set_stencil(int device, const int64_t *c, const double *w, double cs2);
 
+/* Any stencil of Q <= 37 populations (e.g. D2Q9, velocity_set.py:117-124):
+ * the reference D2Q37 ordering selects the specialised kernels, anything
+ * else the generic per-population kernels (csrc/generic.cuh: the reference
+ * arithmetic, bitwise; "fast" falls back to it).  Built for Q = 9 and 37. */
+int tlb_set_stencil_q(int device, int q, const int64_t *c, const double *w,
+                      double cs2);
+/* test hook: run the D2Q37 stencil through the generic kernels (1) or the
+ * specialised ones (0) */
+int tlb_force_generic(int device, int on);
+
 /* propagate (pull)      replaces kernels.propagate, kernels.py:168-177 */
 int tlb_propagate(const TlbField *prv, const TlbField *nxt, TlbRegion r,
                   tlb_stream_t stream);

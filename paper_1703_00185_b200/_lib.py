@@ -71,6 +71,8 @@ SIGNATURES = [
     ("tlb_set_device", _INT, [_INT]),
     ("tlb_device_count", _INT, []),
     ("tlb_set_stencil", _INT, [_INT, _P, _P, ctypes.c_double]),
+    ("tlb_set_stencil_q", _INT, [_INT, _INT, _P, _P, ctypes.c_double]),
+    ("tlb_force_generic", _INT, [_INT, _INT]),
     ("tlb_propagate", _INT, [_FP, _FP, TlbRegion, _P]),
     ("tlb_bc", _INT, [_FP, _PP, _INT, _INT, _I32, _I32, _P, _P]),
     ("tlb_collide", _INT, [_FP, _FP, TlbRegion, _PP, _INT, _P, _P]),
@@ -157,18 +159,17 @@ def torch_cuda():
 
 
 def ensure_stencil(vs, device):
-    """Upload vs's constants to `device` once (tlb_set_stencil)."""
-    if vs.Q != 37:
-        raise UnsupportedCaseError(
-            f"{vs.name}: the sm_100a kernels are specialised for D2Q37")
+    """Upload vs's constants to `device` when they change (tlb_set_stencil_q):
+    the reference D2Q37 ordering runs the specialised kernels, other stencils
+    (D2Q9) the generic ones."""
     key = (int(device), vs.c.tobytes(), vs.w.tobytes(), float(vs.cs2))
     if _stencil_devices.get(int(device)) == key:
         return
     lib = load()
     c = np.ascontiguousarray(vs.c, dtype=np.int64)
     w = np.ascontiguousarray(vs.w, dtype=np.float64)
-    check(lib.tlb_set_stencil(int(device), c.ctypes.data, w.ctypes.data, float(vs.cs2)),
-          "set_stencil")
+    check(lib.tlb_set_stencil_q(int(device), int(vs.Q), c.ctypes.data, w.ctypes.data,
+                                float(vs.cs2)), "set_stencil")
     _stencil_devices[int(device)] = key
 
 
@@ -189,9 +190,10 @@ def field(t, Lx=None, Ly=None, H=0, Hy=None):
     return TlbField(t.data_ptr(), sl, sx, sy, Lx, Ly, Hx, Hy)
 
 
-def params(p):
-    """TlbParams from a PhysicsParams."""
-    order = p.eq_order if p.eq_order is not None else 4
+def params(p, vs=None):
+    """TlbParams from a PhysicsParams; eq_order None means the stencil's own
+    order (kernels.py:80-81: 4 for D2Q37, 2 for D2Q9)."""
+    order = p.eq_order if p.eq_order is not None else (vs.eq_order if vs is not None else 4)
     arith = ARITH.get(getattr(p, "arith", "exact"))
     if arith is None:
         raise DomainError(f"unknown arith mode {p.arith!r}")

@@ -359,9 +359,13 @@ __global__ void __launch_bounds__(128, MINB) k_site(const __grid_constant__ Site
     }
 }
 
+// generic-stencil path (D2Q9, ...), dispatched from the launchers below
+#include "generic.cuh"
+
 // --------------------------------------------------------------- launcher --
 template <int KIND, bool INPLACE>
 static int launch_site(SiteLaunch &L, bool exact, int order, cudaStream_t s, const char *what) {
+    if (device_generic()) return launch_gen<KIND, INPLACE>(L, gen_host().Q, s, what);
     const int bs = 128;
     constexpr bool gather = KIND == K_PROPAGATE || KIND == K_FUSED;
     for (int l = 0; l < Q; ++l) {
@@ -501,10 +505,10 @@ static void wall_rows(SiteLaunch &L, const TlbField *f, int flags) {
 }
 
 // --------------------------------------------------------- small kernels --
-__global__ void k_extend_walls(Fld f, int NX, int upper, int lower) {
-    // grid: (ceil(NX*Q/128)); each thread one (l, x) column, copies 2*Hy cells
+__global__ void k_extend_walls(Fld f, int NX, int nq, int upper, int lower) {
+    // grid: (ceil(NX*nq/128)); each thread one (l, x) column, copies 2*Hy cells
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= (long long)NX * Q) return;
+    if (i >= (long long)NX * nq) return;
     const int l = (int)(i / NX), x = (int)(i % NX);
     double *col = f.base + (long long)l * f.sl + (long long)x * f.sx;
     const double top = col[(long long)(f.Hy + f.Ly - 1) * f.sy];
@@ -522,11 +526,13 @@ struct FaceLines {
 };
 
 static FaceLines face_lines(int sign, int axis) {
+    // face plans of the device's stencil (runtime.py:94-107)
+    const GenHost &g = gen_host();
     FaceLines t;
     t.n = 0;
     for (int d = 1; d <= 3; ++d)
-        for (int l = 0; l < Q; ++l) {
-            int c = axis == 0 ? CX(l) : CY(l);
+        for (int l = 0; l < g.Q; ++l) {
+            int c = axis == 0 ? g.cx[l] : g.cy[l];
             if (sign * c >= d) {
                 t.l[t.n] = l;
                 t.d[t.n] = d;
@@ -749,6 +755,46 @@ int tlb_device_count(void) {
     return n;
 }
 
+// generic tables (every stencil) -- ex/ey/q with the expressions of
+// kernels.py:87-97
+static int set_generic(int device, int nq, const int64_t *c, const double *w, double cs2) {
+    if (nq < 1 || nq > GQ) return fail(TLB_ERR_UNSUPPORTED, "Q=%d: at most %d populations", nq, GQ);
+    GenConst g;
+    memset(&g, 0, sizeof g);
+    g.Q = nq;
+    g.cs2 = cs2;
+    g.cs = std::sqrt(cs2);
+    GenHost &hst = g_gen[device];
+    hst.Q = nq;
+    for (int l = 0; l < nq; ++l) {
+        g.cx[l] = hst.cx[l] = (int)c[2 * l];
+        g.cy[l] = hst.cy[l] = (int)c[2 * l + 1];
+        g.w[l] = w[l];
+        g.ex[l] = (double)c[2 * l] / g.cs;
+        g.ey[l] = (double)c[2 * l + 1] / g.cs;
+        g.q[l] = g.ex[l] * g.ex[l] + g.ey[l] * g.ey[l];
+    }
+    TLB_CUDA_CHECK(cudaSetDevice(device));
+    TLB_CUDA_CHECK(cudaDeviceSynchronize());  // no kernel may still read the old table
+    TLB_CUDA_CHECK(cudaMemcpyToSymbol(G, &g, sizeof g));
+    return TLB_OK;
+}
+
+int tlb_set_stencil_q(int device, int nq, const int64_t *c, const double *w, double cs2) {
+    if (!c || !w) return fail(TLB_ERR_CONTRACT, "null stencil");
+    if (device < 0 || device >= 64) return fail(TLB_ERR_CONTRACT, "bad device %d", device);
+    bool d2q37 = nq == Q;
+    for (int l = 0; d2q37 && l < Q; ++l)
+        d2q37 = c[2 * l] == CX(l) && c[2 * l + 1] == CY(l);
+    if (d2q37) return tlb_set_stencil(device, c, w, cs2);
+    int e = set_generic(device, nq, c, w, cs2);
+    if (e) return e;
+    TLB_CUDA_CHECK(cudaDeviceSynchronize());
+    g_qdev[device] = nq;
+    g_stencil_set[device] = true;
+    return TLB_OK;
+}
+
 int tlb_set_stencil(int device, const int64_t *c, const double *w, double cs2) {
     if (!c || !w) return fail(TLB_ERR_CONTRACT, "null stencil");
     for (int l = 0; l < Q; ++l)
@@ -780,9 +826,22 @@ int tlb_set_stencil(int device, const int64_t *c, const double *w, double cs2) {
     h.set = 1;
     if (device < 0 || device >= 64) return fail(TLB_ERR_CONTRACT, "bad device %d", device);
     TLB_CUDA_CHECK(cudaSetDevice(device));
+    TLB_CUDA_CHECK(cudaDeviceSynchronize());  // no kernel may still read the old table
     TLB_CUDA_CHECK(cudaMemcpyToSymbol(C, &h, sizeof h));
+    int e = set_generic(device, Q, c, w, cs2);
+    if (e) return e;
     TLB_CUDA_CHECK(cudaDeviceSynchronize());
+    g_qdev[device] = Q;
     g_stencil_set[device] = true;
+    return TLB_OK;
+}
+
+// Test hook: route the D2Q37 stencil of `device` through the generic kernels
+// (1) or back to the specialised ones (0) -- they must agree bit for bit.
+int tlb_force_generic(int device, int on) {
+    if (device < 0 || device >= 64 || !g_stencil_set[device] || g_gen[device].Q != Q)
+        return fail(TLB_ERR_STENCIL, "D2Q37 stencil not set on device %d", device);
+    g_qdev[device] = on ? -Q : Q;
     return TLB_OK;
 }
 
@@ -900,8 +959,19 @@ int tlb_moments(const TlbField *f, TlbRegion r, double *rho, double *ux, double 
     const long long n = (long long)(r.x1 - r.x0) * ny;
     if (n <= 0) return TLB_OK;
     Fld d = mkfld(f);
-    k_moments<true><<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
-        d, r.x0, r.y0, ny, n, rho, ux, uy, T, ld, check, status);
+    const unsigned nb = (unsigned)((n + 127) / 128);
+    cudaStream_t s = (cudaStream_t)stream;
+    if (device_generic()) {
+        const int nq = gen_host().Q;
+        if (nq == 9)
+            k_gen_moments<9><<<nb, 128, 0, s>>>(d, r.x0, r.y0, ny, n, rho, ux, uy, T, ld, check, status);
+        else if (nq == 37)
+            k_gen_moments<37><<<nb, 128, 0, s>>>(d, r.x0, r.y0, ny, n, rho, ux, uy, T, ld, check, status);
+        else
+            return fail(TLB_ERR_UNSUPPORTED, "moments: Q=%d", nq);
+        return launch_check("moments");
+    }
+    k_moments<true><<<nb, 128, 0, s>>>(d, r.x0, r.y0, ny, n, rho, ux, uy, T, ld, check, status);
     return launch_check("moments");
 }
 
@@ -914,6 +984,16 @@ int tlb_equilibrium(const double *rho, const double *ux, const double *uy, const
     if (n <= 0) return TLB_OK;
     const unsigned nb = (unsigned)((n + 127) / 128);
     cudaStream_t s = (cudaStream_t)stream;
+    if (device_generic()) {
+        const int nq = gen_host().Q;
+        if (nq == 9)
+            k_gen_equilibrium<9><<<nb, 128, 0, s>>>(rho, ux, uy, T, n, order, out, ld, check, status);
+        else if (nq == 37)
+            k_gen_equilibrium<37><<<nb, 128, 0, s>>>(rho, ux, uy, T, n, order, out, ld, check, status);
+        else
+            return fail(TLB_ERR_UNSUPPORTED, "equilibrium: Q=%d", nq);
+        return launch_check("equilibrium");
+    }
 #define TLB_E(E, O) k_equilibrium<E, O><<<nb, 128, 0, s>>>(rho, ux, uy, T, n, out, ld, check, status)
     if (arith == TLB_ARITH_EXACT) {
         if (order == 4) TLB_E(true, 4); else if (order == 3) TLB_E(true, 3); else TLB_E(true, 2);
@@ -937,16 +1017,25 @@ int tlb_count_negative(const TlbField *f, TlbRegion r, TlbStatus *status, tlb_st
     const int ny = r.y1 - r.y0;
     const long long n = (long long)(r.x1 - r.x0) * ny;
     if (n <= 0) return TLB_OK;
-    k_count_negative<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
-        mkfld(f), r.x0, r.y0, ny, n, status);
+    const unsigned nb = (unsigned)((n + 127) / 128);
+    cudaStream_t s = (cudaStream_t)stream;
+    if (device_generic()) {
+        const int nq = gen_host().Q;
+        if (nq == 9) k_gen_count_negative<9><<<nb, 128, 0, s>>>(mkfld(f), r.x0, r.y0, ny, n, status);
+        else if (nq == 37) k_gen_count_negative<37><<<nb, 128, 0, s>>>(mkfld(f), r.x0, r.y0, ny, n, status);
+        else return fail(TLB_ERR_UNSUPPORTED, "count_negative: Q=%d", nq);
+        return launch_check("count_negative");
+    }
+    k_count_negative<<<nb, 128, 0, s>>>(mkfld(f), r.x0, r.y0, ny, n, status);
     return launch_check("count_negative");
 }
 
 int tlb_extend_walls(const TlbField *f, int upper, int lower, tlb_stream_t stream) {
     const int NX = f->Lx + 2 * f->Hx;
-    const long long n = (long long)NX * Q;
-    k_extend_walls<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(mkfld(f), NX,
-                                                                                  upper, lower);
+    const int nq = device_generic() ? gen_host().Q : Q;
+    const long long n = (long long)NX * nq;
+    k_extend_walls<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
+        mkfld(f), NX, nq, upper, lower);
     return launch_check("extend_walls");
 }
 

@@ -221,6 +221,7 @@ int tlb_peer_step(tlb_peer_t pr, const TlbField *prv, const TlbField *nxt, int p
     if ((e = check_stencil())) return e;
     if ((e = check_params(p))) return e;
     if (p->order != 4) return fail(TLB_ERR_UNSUPPORTED, "peer step: order 4 only");
+    if (device_generic()) return fail(TLB_ERR_UNSUPPORTED, "peer step: D2Q37 kernels only");
     if (flags & (TLB_F_WRAP_X)) return fail(TLB_ERR_CONTRACT, "peer step: X halos are remote");
     const int h = TLB_WALL_ROWS;
     if (prv->Lx < 2 * h + 1) return fail(TLB_ERR_UNSUPPORTED, "peer step: tile narrower than 7");

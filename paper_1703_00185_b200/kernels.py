@@ -75,7 +75,7 @@ def _to_device(a, like=None):
             a = a.cuda()
         return a.to(torch.float64), False
     dev = like.device if like is not None else torch.device("cuda", torch.cuda.current_device())
-    return torch.as_tensor(np.asarray(a, dtype=np.float64), device=dev), True
+    return torch.as_tensor(np.array(a, dtype=np.float64), device=dev), True
 
 
 def _block3(t):
@@ -225,7 +225,7 @@ def collide(f, params: PhysicsParams, vs: VelocitySet):
     st.reset()
     r = _lib.region(0, b.shape[1], 0, b.shape[2])
     _lib.check(_lib.load().tlb_collide(_lib.field(b), _lib.field(out), r,
-                                       _lib.params(params), 0, st.ptr,
+                                       _lib.params(params, vs), 0, st.ptr,
                                        _lib.stream_ptr()), "collide")
     _raise_status(st, "collide")
     return _out(out.reshape(t.shape), np_in)
@@ -262,7 +262,7 @@ def bc(field: PopulationField, params: PhysicsParams, vs: VelocitySet,
     _vs_device(vs, field.data)
     st = _status(field.device)
     st.reset()
-    _lib.check(_lib.load().tlb_bc(field_desc(field), _lib.params(params), int(top),
+    _lib.check(_lib.load().tlb_bc(field_desc(field), _lib.params(params, vs), int(top),
                                   int(bottom), xs.start, xs.stop, st.ptr,
                                   _lib.stream_ptr()), "bc")
     _raise_status(st, "bc")
@@ -290,7 +290,7 @@ def propagate_collide_fused(prv: PopulationField, nxt: PopulationField,
     st.reset()
     _lib.check(_lib.load().tlb_fused(
         field_desc(prv), field_desc(nxt), _lib.region(xs.start, xs.stop, ys.start, ys.stop),
-        _lib.params(params), 0, st.ptr, _lib.stream_ptr()), "fused")
+        _lib.params(params, vs), 0, st.ptr, _lib.stream_ptr()), "fused")
     _raise_status(st, "fused")
 
 

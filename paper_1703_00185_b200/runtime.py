@@ -399,7 +399,7 @@ class RankWorker:
             # order the allocations' zero-fills before any work on our stream
             self.stream.wait_stream(torch.cuda.current_stream(self.device))
         self.plans = face_plans(vs, halo)
-        self.tparams = _lib.params(params)
+        self.tparams = _lib.params(params, vs)
         self._records = []
         self._retained = []
         self._metrics = []

@@ -182,6 +182,33 @@ def main():
     np.savez(os.path.join(HERE, "io.npz"), T=T, pgm=np.frombuffer(pgm, dtype=np.uint8),
              macro_small=r["rt_f20_macro"][:, :4, :3], csv=np.array(csv_txt))
 
+    # ---------------------------------------------------------- D2Q9 --
+    v9 = build_velocity_set("D2Q9")
+    g9 = LatticeGeometry(8, 8, 3, 3, 9)
+    d9 = {}
+    prv, nxt = allocate_field(g9, v9)
+    prv.pops[...] = random_state(g9, v9, seed=29)
+    periodic_fill(prv)
+    d9["prv"] = prv.pops.copy()
+    propagate(prv, nxt, v9)
+    d9["prop"] = nxt.pops.copy()
+    p9 = PhysicsParams(tau=0.8, gx=2e-5, gy=-1e-4, Twall_top=0.3, Twall_bot=0.36)
+    d9["params"] = np.array([p9.tau, p9.gx, p9.gy, p9.dt, p9.Twall_top, p9.Twall_bot])
+    b9 = type(nxt)(g9, "nxt", nxt.pops.copy())
+    bc(b9, p9, v9)
+    d9["bc"] = b9.pops.copy()
+    d9["collide"] = collide(nxt.pops[:, g9.phys_x, g9.phys_y], p9, v9)
+    fz = type(nxt)(g9, "nxt")
+    propagate_collide_fused(prv, fz, p9, v9, (slice(4, 10), slice(5, 9)))
+    d9["fused"] = fz.pops.copy()
+    kw9 = dict(Lx=16, Ly=12, model="D2Q9", params=p9, init="random", init_kwargs={"seed": 4})
+    d9["run_f0"] = run(SimConfig(Np=1, steps=0, **kw9)).populations
+    one9 = run(SimConfig(Np=1, schedule="staged", steps=10, **kw9))
+    two9 = run(SimConfig(Np=2, tiling="1d", schedule="overlapped", steps=10, **kw9))
+    assert np.array_equal(one9.populations, two9.populations)
+    d9["run_f10"] = one9.populations
+    np.savez_compressed(os.path.join(HERE, "d2q9.npz"), **d9)
+
     # -------------------------------------------------------- planner --
     from thermolb import planner as P
     rng = np.random.default_rng(0)
