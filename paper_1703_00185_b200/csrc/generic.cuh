@@ -154,7 +154,8 @@ __device__ __forceinline__ void gen_body(const SiteLaunch &L, int x, int y, bool
     if (KIND == K_BC || KIND == K_FUSED) {
         const bool bot = y >= L.bot_lo && y < L.bot_hi;
         const bool top = y >= L.top_lo && y < L.top_hi;
-        if (bot || top) bits |= gen_bc<NQ>(f, bot ? L.P.Tbot : L.P.Ttop, L.P.order);
+        if (bot) bits |= gen_bc<NQ>(f, L.P.Tbot, L.P.order);  // bottom, then top
+        if (top) bits |= gen_bc<NQ>(f, L.P.Ttop, L.P.order);  // (kernels.py:190-203)
     }
     if (KIND == K_COLLIDE || KIND == K_FUSED) bits |= gen_collide<NQ>(f, L.P);
     if (active) {

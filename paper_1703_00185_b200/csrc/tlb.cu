@@ -297,8 +297,12 @@ __device__ __forceinline__ void site_body(const SiteLaunch &L, int x, int y, boo
     if (EDGE && (KIND == K_BC || KIND == K_FUSED)) {
         const bool bot = y >= L.bot_lo && y < L.bot_hi;
         const bool top = y >= L.top_lo && y < L.top_hi;
-        if (bot || top) {
-            const double Tw = bot ? L.P.Tbot : L.P.Ttop;
+        // bottom wall then top wall, like bc() (kernels.py:190-203): a row in
+        // both (Ly < 6) gets the top equilibrium of the bottom-processed state
+#pragma unroll 1
+        for (int side = 0; side < 2; ++side) {
+            if (!(side ? top : bot)) continue;
+            const double Tw = side ? L.P.Ttop : L.P.Tbot;
             RegF rf{f};
             bits |= EXACT ? bc_exact<ORDER>(rf, Tw) : bc_fast<ORDER>(rf, Tw);
         }

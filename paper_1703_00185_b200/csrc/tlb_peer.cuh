@@ -111,8 +111,10 @@ __global__ void __launch_bounds__(128, 4)
     {
         const bool bot = y >= L.bot_lo && y < L.bot_hi;
         const bool top = y >= L.top_lo && y < L.top_hi;
-        if (bot || top) {
-            const double Tw = bot ? L.P.Tbot : L.P.Ttop;
+#pragma unroll 1
+        for (int side = 0; side < 2; ++side) {  // bottom wall, then top (kernels.py:190-203)
+            if (!(side ? top : bot)) continue;
+            const double Tw = side ? L.P.Ttop : L.P.Tbot;
             RegF rf{f};
             bits |= EXACT ? bc_exact<4>(rf, Tw) : bc_fast<4>(rf, Tw);
         }

@@ -280,7 +280,7 @@ def test_run_api_matches_oracle(vs, orc):
     orc.set_stencil(vs.c, vs.w, vs.cs2)
 
 
-@pytest.mark.parametrize("Lx,Ly", [(7, 13), (3, 6), (5, 9), (130, 7)])
+@pytest.mark.parametrize("Lx,Ly", [(7, 13), (3, 6), (5, 9), (130, 7), (9, 4), (8, 5)])
 def test_ragged_sizes_bitwise(vs, orc, Lx, Ly):
     rng = np.random.default_rng(Lx * 100 + Ly)
     f0 = orc.equilibrium(1.0 + 0.01 * rng.standard_normal((Lx, Ly)),
