@@ -200,22 +200,27 @@ def gpu_arm(args, rank, world, local_rank):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
     vs = tl.build_velocity_set("D2Q37")
+    grid = (world, 1)
+    if args.tiling != "1d":
+        grid = tuple(int(v) for v in args.tiling.lower().split("x"))
+        if grid[0] * grid[1] != world:
+            raise SystemExit(f"--tiling {args.tiling} does not match {world} ranks")
     if args.strong:
         # BASELINE configs[3]: fixed 8192x16384 lattice split over the GPUs
         Lx, Ly = 8192, 16384
-        Lx_tile = Lx // world
+        Lx_tile, Ly_tile = Lx // grid[0], Ly // grid[1]
     else:
-        Lx_tile, Ly = args.Lx, args.Ly
-        Lx = Lx_tile * world
+        Lx_tile, Ly_tile = args.Lx, args.Ly
+        Lx, Ly = Lx_tile * grid[0], Ly_tile * grid[1]
     p = tl.PhysicsParams(tau=0.8, gx=0.0, gy=-1e-5, Twall_top=0.9 * vs.cs2,
                          Twall_bot=1.1 * vs.cs2, arith=args.arith)
-    tiles = tl.decompose(Lx, Ly, world, "1d")
+    tiles = tl.decompose(Lx, Ly, world, "1d" if grid[1] == 1 else grid)
     tile = tiles[rank]
     fabric = tl.DistFabric() if world > 1 else tl.Fabric(1)
     w = tl.RankWorker(tile, vs, p, fabric, schedule=args.schedule, device=dev,
                       exchange=args.exchange)
     macro = tl.init.rayleigh_taylor_macro(Lx, Ly, vs)
-    sl = slice(tile.x0, tile.x0 + Lx_tile)
+    sl = (slice(tile.x0, tile.x0 + Lx_tile), slice(tile.y0, tile.y0 + Ly_tile))
     f0 = tl.equilibrium(*[torch.as_tensor(np.ascontiguousarray(a[sl]), device=dev)
                           for a in macro], vs)
     w.load_block(f0)
@@ -290,7 +295,8 @@ def gpu_arm(args, rank, world, local_rank):
 
     # dominant kernel: the fused step over the (bulk) region of this rank
     h = 3
-    kern_sites = (Lx_tile if world == 1 else Lx_tile - 2 * h) * Ly
+    ey = (2 * h if grid[1] > 1 else 0)    # rows of exchanged Y edges (2-D), approx.
+    kern_sites = (Lx_tile if world == 1 else Lx_tile - 2 * h) * (Ly_tile - ey)
     kern_ms = float(np.mean(bulk_ms))
     achieved = BYTES_SITE * kern_sites / (kern_ms * 1e-3) / 1e9
     pk = peaks()
@@ -349,7 +355,7 @@ def gpu_arm(args, rank, world, local_rank):
         if args.probe:
             _lib.check(lib.tlb_bench_dfma(200000, ctypes.byref(fp), _lib.stream_ptr()), "dfma")
         fp64_peak = fp.value / 1e12 if args.probe else float("nan")
-        kern_tflops = (FLOP_SITE * kern_sites + FLOP_WALL_SITE * 6 * Lx_tile) / (kern_ms * 1e-3) / 1e12
+        kern_tflops = (FLOP_SITE * kern_sites) / (kern_ms * 1e-3) / 1e12
         split = split_kernels(w, tl, _lib, field_desc, torch) if args.split else None
         out = {
             "metric": METRIC, "value": round(mlups, 3), "unit": "MLUPS",
@@ -358,14 +364,15 @@ def gpu_arm(args, rank, world, local_rank):
             "scaling": "strong" if args.strong else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (Rayleigh-Taylor initial state, reference init.py:45-64)",
             "config": {"workload": f"D2Q37 RT {Lx}x{Ly}" + (
-                f" (1-D X tiles of {Lx_tile}x{Ly}, overlapped NCCL halo)" if world > 1 else
+                f" ({'1-D X' if grid[1] == 1 else f'{grid[0]}x{grid[1]}'} tiles of "
+                f"{Lx_tile}x{Ly_tile}, overlapped halo exchange)" if world > 1 else
                 (" on 1 B200 (BASELINE configs[3], strong-scaling base)" if args.strong
                  else " on 1 B200 (BASELINE configs[1])")),
-                "Lx": Lx, "Ly": Ly, "tiling": "1d", "schedule": args.schedule,
+                "Lx": Lx, "Ly": Ly, "tiling": args.tiling, "schedule": args.schedule,
                 "arith": args.arith, "tau": 0.8, "gy": -1e-5,
                 "exchange": args.exchange if world > 1 else None,
                 "l2": "no flush: 2 x %.2f GB state per GPU >> 126 MB L2" % (
-                    37 * (Lx_tile + 6) * (Ly + 6) * 8 / 1e9)},
+                    37 * (Lx_tile + 6) * (Ly_tile + 6) * 8 / 1e9)},
             "gflops_fp64": round(gflops, 2),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak,
                          "unit": "GB/s", "frac": round(achieved / hbm_peak, 4),
@@ -395,7 +402,7 @@ def gpu_arm(args, rank, world, local_rank):
         if other:
             out["other_arith"] = other
     # e2e through the public API with host buffers
-    e2e = e2e_run(args, w, tl, torch, dist, local_rank, Lx_tile, Ly) if args.e2e else None
+    e2e = e2e_run(args, w, tl, torch, dist, local_rank, Lx_tile, Ly_tile) if args.e2e else None
     if rank == 0:
         out["e2e"] = e2e
         if world == 1 and args.cpu_seconds > 0:
@@ -511,6 +518,8 @@ def main():
                          "into the step kernel")
     ap.add_argument("--Lx", type=int, default=TILE_LX, help="tile Lx per GPU")
     ap.add_argument("--Ly", type=int, default=TILE_LY)
+    ap.add_argument("--tiling", default="1d",
+                    help="'1d' (north star) or a rank grid 'NXxNY', e.g. 2x2 (paper's 2-D tiling)")
     ap.add_argument("--strong", action="store_true",
                     help="configs[3]: 8192x16384 total, split over the GPUs (strong scaling)")
     ap.add_argument("--preload", type=float, default=1.0, help="s of untimed load for clocks")

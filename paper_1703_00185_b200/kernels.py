@@ -97,7 +97,7 @@ def _vs_device(vs, t):
     _lib.ensure_stencil(vs, t.device.index or 0)
 
 
-def _raise_status(st, what, field_offsets=None):
+def _raise_status(st, what):
     s = st.read()
     if s.flags & _lib.ST_EQ_DOMAIN:
         raise DomainError("equilibrium requires rho > 0 and T > 0")
@@ -123,10 +123,6 @@ def _check_region(geom: LatticeGeometry, region):
 def field_desc(f: PopulationField):
     g = f.geom
     return _lib.field(f.pops, g.Lx, g.Ly, g.Hx, g.Hy)
-
-
-def _sync_check(st, what):
-    _raise_status(st, what)
 
 
 # ------------------------------------------------------------------ moments --

@@ -24,7 +24,6 @@ Both decompositions of the reference are supported: the 1-D X ring (the
 north star) and the 2-D grid (Y chain with walls or Y ring).
 """
 
-import math
 import queue
 import threading
 import time
@@ -34,8 +33,7 @@ import numpy as np
 
 from . import _lib
 from .errors import (ConfigurationError, DeadlockError, DegenerateStateError,
-                     DomainError, ProtocolError, ThermoLBError,
-                     UnsupportedCaseError)
+                     DomainError, ProtocolError, ThermoLBError)
 from .geometry import LatticeGeometry, allocate_field, swap_buffers
 from .kernels import WALL_ROWS, field_desc
 from .velocity_set import VelocitySet
