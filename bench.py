@@ -114,26 +114,39 @@ class ClockSampler:
         except subprocess.TimeoutExpired:
             self.proc.kill()
         self.thread.join(timeout=2)
-        sm, smax, reasons = [], [], set()
-        for r in self.rows:
-            try:
-                util = float(r[7])
-            except ValueError:
-                util = 100.0
-            if util < 50:
-                continue
-            try:
-                sm.append(float(r[0]))
-                smax.append(float(r[1]))
-            except ValueError:
-                continue
-            for name, v in zip(self.NAMES, r[3:7]):
-                if v.lower() == "active":
-                    reasons.add(name)
+        def parse(rows, loaded_only):
+            sm, smax, reasons = [], [], set()
+            for r in rows:
+                try:
+                    util = float(r[7])
+                except ValueError:
+                    util = 100.0
+                try:
+                    power = float(r[2])
+                except ValueError:
+                    power = 1000.0
+                if loaded_only and util < 50 and power < 300:
+                    continue
+                try:
+                    sm.append(float(r[0]))
+                    smax.append(float(r[1]))
+                except ValueError:
+                    continue
+                for name, v in zip(self.NAMES, r[3:7]):
+                    if v.lower() == "active":
+                        reasons.add(name)
+            return sm, smax, reasons
+
+        sm, smax, reasons = parse(self.rows, True)
+        loaded = bool(sm)
+        if not sm:  # no sample classified as under load: report all of them
+            sm, smax, reasons = parse(self.rows, False)
         if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0,
+                    "samples_total": len(self.rows)}
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(smax),
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm),
+                "samples_total": len(self.rows), "under_load": loaded}
 
 
 # ------------------------------------------------------------ CPU oracle --
@@ -522,7 +535,7 @@ def main():
                     help="'1d' (north star) or a rank grid 'NXxNY', e.g. 2x2 (paper's 2-D tiling)")
     ap.add_argument("--strong", action="store_true",
                     help="configs[3]: 8192x16384 total, split over the GPUs (strong scaling)")
-    ap.add_argument("--preload", type=float, default=1.0, help="s of untimed load for clocks")
+    ap.add_argument("--preload", type=float, default=2.0, help="s of untimed load for clocks")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-e2e", dest="e2e", action="store_false")
     ap.add_argument("--no-split", dest="split", action="store_false")
