@@ -277,7 +277,6 @@ int tlb_pgm_image(const double *v, int64_t nx, int64_t ny, int64_t ld,
  * __launch_bounds__ minimum CTAs/SM of the fused kernel (1 = compiler's
  * choice, 4 = default, 5). */
 #define TLB_TUNE_MINBLOCKS 1
-#define TLB_TUNE_RELOAD 2 /* 0 = off; 4/5 = relaxation re-reads f, 4/5 CTAs/SM */
 int tlb_set_tuning(int key, int value);
 
 /* Diagnostics: measured FP64 FMA throughput of this GPU (flop/s, 2 per

@@ -360,21 +360,6 @@ __device__ __forceinline__ bool moments_exact(const F &f, double &rho, double &u
 }
 
 // collide one site in place (kernels.py:139-146).  Returns TLB_ST_* bits.
-// Moments read through `fm`, the relaxation reads/writes through `f` (they
-// may differ: e.g. registers for the moments, a reload for the relaxation).
-template <int ORDER, class FM, class F>
-__device__ __forceinline__ unsigned collide_exact2(const FM &fm, F &f, const Phys &P) {
-    double rho, ux, uy, T;
-    if (!moments_exact(fm, rho, ux, uy, T)) return 1u;
-    const double ub = dadd(ux, P.K1);
-    const double vb = dadd(uy, P.K2);
-    const double Tb = dsub(T, P.K3);
-    if (!(Tb > 0.0)) return 2u;
-    const EqSite e = eq_site_exact(rho, ub, vb, Tb);
-    eq_all_exact<ORDER, 1, F>(f, e, P.omega);
-    return 0u;
-}
-
 template <int ORDER, class F>
 __device__ __forceinline__ unsigned collide_exact(F &f, const Phys &P) {
     double rho, ux, uy, T;

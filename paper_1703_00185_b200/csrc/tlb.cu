@@ -49,7 +49,6 @@ static int launch_check(const char *what) {
 
 static bool g_stencil_set[64];
 static int g_minb = 4;    // tuning: __launch_bounds__ min blocks of the fused kernel
-static int g_reload = 0;  // tuning: relaxation re-reads f (0 = off, 4/5 = on with that occupancy)
 
 // --------------------------------------------------------- device helpers --
 struct Fld {
@@ -257,31 +256,7 @@ struct RegStoreF {
     }
 };
 
-// As RegStoreF, but the relaxation re-reads f_l from global (an L1/L2 hit:
-// the line was fetched for the moments moments ago) instead of keeping the
-// 37-vector live in registers through the equilibrium -- trading a cache
-// re-read for registers, i.e. for ILP in the FP64 chains.
-struct ReloadStoreF {
-    const char *sp;
-    const long long *soffb;
-    char *dp;
-    const long long *doffb;
-    bool active;
-    unsigned neg;
-    __device__ __forceinline__ double get(int l) const {
-        double v;
-        asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(v) : "l"(sp + soffb[l]));
-        return v;
-    }
-    __device__ __forceinline__ void put(int l, double v) {
-        if (active) {
-            *reinterpret_cast<double *>(dp + doffb[l]) = v;
-            neg += v < 0.0;
-        }
-    }
-};
-
-template <int KIND, bool EXACT, int ORDER, bool INPLACE, bool EDGE, bool RELOAD = false>
+template <int KIND, bool EXACT, int ORDER, bool INPLACE, bool EDGE>
 __device__ __forceinline__ void site_body(const SiteLaunch &L, int x, int y, bool active) {
     double f[Q];
     constexpr bool gather = KIND == K_PROPAGATE || KIND == K_FUSED;
@@ -307,18 +282,6 @@ __device__ __forceinline__ void site_body(const SiteLaunch &L, int x, int y, boo
             bits |= EXACT ? bc_exact<ORDER>(rf, Tw) : bc_fast<ORDER>(rf, Tw);
         }
     }
-    if constexpr (RELOAD && !EDGE && !INPLACE && (KIND == K_COLLIDE || KIND == K_FUSED)) {
-        char *dp = reinterpret_cast<char *>(L.dst.base + (long long)x * L.dst.sx +
-                                            (long long)y * L.dst.sy);
-        const char *sp = reinterpret_cast<const char *>(
-            L.src.base + (long long)x * L.src.sx + (long long)y * L.src.sy);
-        RegF fm{f};
-        ReloadStoreF sf{sp, L.soffb, dp, L.doffb, active, 0u};
-        bits |= EXACT ? collide_exact2<ORDER>(fm, sf, L.P) : collide_fast2<ORDER>(fm, sf, L.P);
-        if (active) report(L.status, bits, x, y, L.step);
-        if (L.flags & TLB_F_COUNT_NEG) count_neg_n(L.status, sf.neg);
-        return;
-    }
     if constexpr (!EDGE && !INPLACE && (KIND == K_COLLIDE || KIND == K_FUSED)) {
         char *dp = reinterpret_cast<char *>(L.dst.base + (long long)x * L.dst.sx +
                                             (long long)y * L.dst.sy);
@@ -342,7 +305,7 @@ __device__ __forceinline__ void site_body(const SiteLaunch &L, int x, int y, boo
 // One thread = one site.  Sites are enumerated y-fastest inside each
 // rectangle so consecutive lanes touch consecutive addresses of every
 // population plane.
-template <int KIND, bool EXACT, int ORDER, bool INPLACE, int MINB, bool RELOAD = false>
+template <int KIND, bool EXACT, int ORDER, bool INPLACE, int MINB>
 __global__ void __launch_bounds__(128, MINB) k_site(const __grid_constant__ SiteLaunch L) {
     if (blockIdx.x < L.nfb) {
         const unsigned total = L.fr_end[3];
@@ -358,7 +321,7 @@ __global__ void __launch_bounds__(128, MINB) k_site(const __grid_constant__ Site
         const unsigned i = (blockIdx.x - L.nfb) * blockDim.x + threadIdx.x;
         const bool active = i < L.in.n;
         const unsigned ii = active ? i : L.in.n - 1;
-        site_body<KIND, EXACT, ORDER, INPLACE, false, RELOAD>(
+        site_body<KIND, EXACT, ORDER, INPLACE, false>(
             L, L.in.x0 + (int)(ii / L.in.ny), L.in.y0 + (int)(ii % L.in.ny), active);
     }
 }
@@ -389,9 +352,7 @@ static int launch_site(SiteLaunch &L, bool exact, int order, cudaStream_t s, con
 #define TLB_L(E, O) k_site<KIND, E, O, INPLACE, 4><<<grid, block, 0, s>>>(L)
 #define TLB_LT(E, O)                                                               \
     do {                                                                           \
-        if (g_reload == 4) k_site<KIND, E, O, INPLACE, 4, true><<<grid, block, 0, s>>>(L); \
-        else if (g_reload == 5) k_site<KIND, E, O, INPLACE, 5, true><<<grid, block, 0, s>>>(L); \
-        else if (g_minb == 1) k_site<KIND, E, O, INPLACE, 1><<<grid, block, 0, s>>>(L); \
+        if (g_minb == 1) k_site<KIND, E, O, INPLACE, 1><<<grid, block, 0, s>>>(L); \
         else if (g_minb == 5) k_site<KIND, E, O, INPLACE, 5><<<grid, block, 0, s>>>(L); \
         else TLB_L(E, O);                                                          \
     } while (0)
@@ -732,12 +693,6 @@ int tlb_set_tuning(int key, int value) {
         if (value != 1 && value != 4 && value != 5)
             return fail(TLB_ERR_CONTRACT, "min blocks must be 1, 4 or 5");
         g_minb = value;
-        return TLB_OK;
-    }
-    if (key == TLB_TUNE_RELOAD) {
-        if (value != 0 && value != 4 && value != 5)
-            return fail(TLB_ERR_CONTRACT, "reload must be 0, 4 or 5");
-        g_reload = value;
         return TLB_OK;
     }
     return fail(TLB_ERR_CONTRACT, "unknown tuning key %d", key);

@@ -74,9 +74,6 @@ def main():
             lib.tlb_set_tuning(key, default)
             return r
         return run
-    for rl in (4, 5):
-        variants[f"fused_exact_step_neg_reload{rl}"] = tuned(variants["fused_exact_step_neg"], 2, rl, 0)
-        variants[f"fused_fast_step_reload{rl}"] = tuned(variants["fused_fast_step"], 2, rl, 0)
     for mb in (1, 5):
         variants[f"fused_exact_step_neg_minb{mb}"] = tuned(variants["fused_exact_step_neg"], 1, mb, 4)
         variants[f"fused_fast_step_minb{mb}"] = tuned(variants["fused_fast_step"], 1, mb, 4)
