@@ -246,13 +246,14 @@ struct RegStoreF {
     unsigned neg;
     __device__ __forceinline__ double get(int l) const { return a[l]; }
     __device__ __forceinline__ void put(int l, double v) {
-        if (active) {
-            if constexpr (STREAM)
-                __stcs(reinterpret_cast<double *>(dp + doffb[l]), v);
-            else
-                *reinterpret_cast<double *>(dp + doffb[l]) = v;
-            neg += v < 0.0;
+        // predicated store, branch-free count (no reconvergence per output)
+        double *p = reinterpret_cast<double *>(dp + doffb[l]);
+        if constexpr (STREAM) {
+            if (active) __stcs(p, v);
+        } else {
+            if (active) *p = v;
         }
+        neg += (unsigned)(active & (v < 0.0));
     }
 };
 
