@@ -144,9 +144,16 @@ class ClockSampler:
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0,
                     "samples_total": len(self.rows)}
+        power = []
+        for r in self.rows:
+            try:
+                power.append(float(r[2]))
+            except ValueError:
+                pass
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(smax),
                 "reasons": sorted(reasons), "samples": len(sm),
-                "samples_total": len(self.rows), "under_load": loaded}
+                "samples_total": len(self.rows), "under_load": loaded,
+                "power_w_median": float(np.median(power)) if power else None}
 
 
 # ------------------------------------------------------------ CPU oracle --
@@ -403,6 +410,12 @@ def gpu_arm(args, rank, world, local_rank):
                                   "frac": round(kern_tflops / fp64_peak, 4),
                                   "flops_per_site": FLOP_SITE}},
             "clocks": clocks,
+            "energy": ({"uJ_per_site_update": round(clocks["power_w_median"] * world /
+                                                    (mlups * 1e6) * 1e6, 5),
+                        "basis": "median nvidia-smi power.draw of rank 0's GPU during the "
+                                 "pre-load + timed steps x n_gpus / MLUPS (paper Table 3 "
+                                 "reports TDP-based uJ/site)"}
+                       if clocks and clocks.get("power_w_median") else None),
             "host_enqueue_ms_per_step": round(host_ms, 4),
             "gpu_launches": args.steps * (1 if world == 1 else
                                           (2 if args.exchange == "p2p" else 4)),

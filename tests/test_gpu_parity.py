@@ -317,3 +317,16 @@ def test_error_surfaces_with_step(vs):
     w.step(0)
     with pytest.raises(tl.DomainError):
         w.collect()
+
+
+def test_rt256_1000_steps_exact_bitwise_and_fast_drift(vs, runs, rt256, orc):
+    """1000 RT steps: exact stays bitwise equal to the oracle; fast stays
+    within the north star's 1e-12 relative contract."""
+    p6 = orc.params6(*runs["rt_params"])
+    want, _ = orc.run(rt256, 1000, p6)
+    got, _ = _run(vs, rt256, 1000, P(runs["rt_params"]), "overlapped")
+    assert np.array_equal(got, want)
+    fast, _ = _run(vs, rt256, 1000, P(runs["rt_params"], arith="fast"), "overlapped")
+    rel = np.max(np.abs(fast - want) / np.abs(want))
+    print("fast drift after 1000 steps:", rel)
+    assert rel < 1e-12
