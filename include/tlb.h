@@ -221,6 +221,11 @@ int tlb_nccl_unique_id(char *out128);
 int tlb_ring_create(const char *uid128, int nranks, int rank, int device,
                     tlb_ring_t *out);
 int tlb_ring_destroy(tlb_ring_t ring);
+/* Failure detection (runtime.py:146-160 analog): the communicator's async
+ * NCCL error (0 = ncclSuccess), and an abort that releases stalled NCCL
+ * kernels so a rank that timed out can raise and exit. */
+int tlb_ring_async_error(tlb_ring_t ring, int *nccl_result);
+int tlb_ring_abort(tlb_ring_t ring);
 /* 2-D tiling (decompose, runtime.py:54-91): neighbour ranks in the NCCL
  * communicator; -1 = none (wall side).  With up/down neighbours the step
  * exchanges Y faces first (physical columns), then X faces (full height, so

@@ -96,6 +96,8 @@ SIGNATURES = [
     ("tlb_nccl_unique_id", _INT, [ctypes.c_char_p]),
     ("tlb_ring_create", _INT, [ctypes.c_char_p, _INT, _INT, _INT, ctypes.POINTER(_P)]),
     ("tlb_ring_destroy", _INT, [_P]),
+    ("tlb_ring_async_error", _INT, [_P, ctypes.POINTER(_INT)]),
+    ("tlb_ring_abort", _INT, [_P]),
     ("tlb_ring_set_neighbors", _INT, [_P, _INT, _INT, _INT, _INT, _P]),
     ("tlb_ring_exchange", _INT, [_P, _FP, _INT, _P, _P, _P]),
     ("tlb_ring_step", _INT, [_P, _FP, _FP, _PP, _INT, _P, _P, _P, _P, _P, _P]),

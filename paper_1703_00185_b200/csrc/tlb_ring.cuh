@@ -38,6 +38,7 @@ struct Nccl {
     ncclResult_t (*GroupStart)() = nullptr;
     ncclResult_t (*GroupEnd)() = nullptr;
     const char *(*GetErrorString)(ncclResult_t) = nullptr;
+    ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t *) = nullptr;
 };
 
 static Nccl &nccl() {
@@ -58,7 +59,7 @@ static Nccl &nccl() {
     }
         TLB_SYM(GetVersion) TLB_SYM(GetUniqueId) TLB_SYM(CommInitRank) TLB_SYM(CommDestroy)
         TLB_SYM(CommAbort) TLB_SYM(Send) TLB_SYM(Recv) TLB_SYM(GroupStart) TLB_SYM(GroupEnd)
-        TLB_SYM(GetErrorString)
+        TLB_SYM(GetErrorString) TLB_SYM(CommGetAsyncError)
 #undef TLB_SYM
         n.ok = true;
     });
@@ -216,12 +217,30 @@ int tlb_ring_destroy(tlb_ring_t r) {
     if (!r) return TLB_OK;
     auto &N = tlbring::nccl();
     cudaSetDevice(r->device);
-    if (r->side) cudaStreamSynchronize(r->side);
+    if (r->comm && r->side) cudaStreamSynchronize(r->side);
     if (r->comm && N.ok) N.CommDestroy(r->comm);
     if (r->ev_pack) cudaEventDestroy(r->ev_pack);
     if (r->ev_done) cudaEventDestroy(r->ev_done);
     if (r->side) cudaStreamDestroy(r->side);
     delete r;
+    return TLB_OK;
+}
+
+int tlb_ring_async_error(tlb_ring_t r, int *nccl_result) {
+    if (!r || !r->comm) return fail(TLB_ERR_CONTRACT, "null ring");
+    ncclResult_t res = ncclSuccess;
+    TLB_NCCL_CHECK(tlbring::nccl().CommGetAsyncError(r->comm, &res));
+    *nccl_result = (int)res;
+    return TLB_OK;
+}
+
+// Abort the communicator (a stalled or failed peer): outstanding NCCL
+// kernels are released so the process can report the failure and exit.
+int tlb_ring_abort(tlb_ring_t r) {
+    if (!r || !r->comm) return TLB_OK;
+    auto &N = tlbring::nccl();
+    if (N.ok) N.CommAbort(r->comm);
+    r->comm = nullptr;
     return TLB_OK;
 }
 

@@ -264,6 +264,21 @@ class DistFabric:
             _lib.load().tlb_ring_destroy(self._ring)
             self._ring = None
 
+    def abort_ring(self):
+        """Release NCCL kernels stalled on a dead or late peer."""
+        if self._ring is not None:
+            _lib.load().tlb_ring_abort(self._ring)
+
+    def async_error(self):
+        """The ring communicator's asynchronous NCCL error code (0 = none)."""
+        import ctypes
+        if self._ring is None:
+            return 0
+        code = ctypes.c_int(0)
+        _lib.check(_lib.load().tlb_ring_async_error(self._ring, ctypes.byref(code)),
+                   "nccl async error")
+        return code.value
+
     def start_face(self, w, step, axis, out_plus, out_minus):
         dist = self.dist
         nb = w.tile.neighbors
@@ -762,8 +777,29 @@ class RankWorker:
         self.prv, self.nxt = swap_buffers(self.prv, self.nxt)
 
     # -- results -------------------------------------------------------------
-    def synchronize(self):
-        self.stream.synchronize()
+    def synchronize(self, timeout=None):
+        """Wait for this rank's queued steps.  With a fabric timeout (one
+        process per GPU) a rank that waits longer than `timeout` seconds --
+        a stalled or failed ring neighbour -- aborts the NCCL ring and raises
+        DeadlockError naming itself (runtime.py:146-149)."""
+        torch = _lib.torch_cuda()
+        if timeout is None:
+            timeout = getattr(self.fabric, "timeout", None) if isinstance(
+                self.fabric, DistFabric) else None
+        if not timeout:
+            self.stream.synchronize()
+            return
+        ev = torch.cuda.Event()
+        ev.record(self.stream)
+        deadline = time.monotonic() + timeout
+        while not ev.query():
+            if time.monotonic() > deadline:
+                err = self.fabric.async_error()
+                self.fabric.abort_ring()
+                raise DeadlockError(f"rank {self.tile.rank} stalled for {timeout:.0f} s waiting "
+                                    f"for its ring neighbours (NCCL async error {err})",
+                                    rank=self.tile.rank)
+            time.sleep(2e-4)
 
     def close(self):
         """Release the peer mappings (after every rank finished its steps)."""

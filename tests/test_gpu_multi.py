@@ -41,6 +41,20 @@ def test_torchrun_nccl_ring_bitwise(n):
     assert "DIST OK" in out.stdout
 
 
+def test_torchrun_stalled_neighbour_raises_deadlock():
+    """A rank whose ring neighbour stops stepping times out, aborts the NCCL
+    ring and raises DeadlockError instead of hanging (tests/dist_stall.py)."""
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           "--nproc-per-node=2", "--master-addr", "127.0.0.1",
+           "--master-port", str(_port()), os.path.join(ROOT, "tests", "dist_stall.py")]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=180, cwd=ROOT)
+    print(out.stdout[-3000:], out.stderr[-3000:])
+    assert out.returncode == 0
+    assert "STALL OK" in out.stdout
+
+
 def test_inprocess_ranks_on_two_gpus(orc):
     vs = tl.build_velocity_set("D2Q37")
     orc.set_stencil(vs.c, vs.w, vs.cs2)
