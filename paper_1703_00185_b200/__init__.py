@@ -12,7 +12,7 @@ from .errors import (AllocationError, ConfigurationError, ContractViolation,
                      DeadlockError, DegenerateStateError, DeviceError,
                      DomainError, ProtocolError, ThermoLBError,
                      UnsupportedCaseError)
-from .geometry import (AOS, SOA, LatticeGeometry, MacroFields, PopulationField,
+from .geometry import (AOS, COLUMN, SOA, LatticeGeometry, MacroFields, PopulationField,
                        allocate_field, site_index, swap_buffers)
 from .kernels import (WALL_ROWS, PhysicsParams, apply_shift, bc, collide,
                       count_negative, equilibrium, moments, propagate,
@@ -23,7 +23,7 @@ from .sim import RunResult, SimConfig, run
 from .velocity_set import VelocitySet, build_velocity_set
 
 __all__ = [
-    "AOS", "SOA", "LatticeGeometry", "MacroFields", "PopulationField",
+    "AOS", "COLUMN", "SOA", "LatticeGeometry", "MacroFields", "PopulationField",
     "allocate_field", "site_index", "swap_buffers",
     "PhysicsParams", "apply_shift", "bc", "collide", "equilibrium", "moments",
     "propagate", "propagate_collide_fused", "count_negative", "WALL_ROWS",

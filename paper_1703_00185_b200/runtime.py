@@ -347,7 +347,7 @@ class RankWorker:
     _RING = 1024
 
     def __init__(self, tile, vs, params, fabric=None, schedule="staged", walls=True,
-                 layout="soa", halo=DEFAULT_HALO, debug_poison=False, device=None,
+                 layout="column", halo=DEFAULT_HALO, debug_poison=False, device=None,
                  periodic_y=False, exchange="nccl", timing="sampled", timing_every=32):
         torch = _lib.torch_cuda()
         if schedule not in ("staged", "overlapped"):

@@ -39,7 +39,7 @@ class SimConfig:
         default_factory=lambda: PhysicsParams(tau=1.0, gx=0.0, gy=-1e-4))
     walls: bool = True
     periodic_y: bool = False
-    layout: str = "soa"
+    layout: str = "column"   # storage order only; results are layout-independent
     halo: int = DEFAULT_HALO
     init: str = "uniform"
     init_kwargs: dict = field(default_factory=dict)

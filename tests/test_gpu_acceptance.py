@@ -242,14 +242,30 @@ def test_staged_equals_overlapped(vs):
     assert np.array_equal(a.populations, b.populations)
 
 
-def test_aos_layout_same_bits(vs):
-    """Layouts are storage only: AoS fields give the SoA bits (geometry.py:1-7)."""
+@pytest.mark.parametrize("tiling,periodic", [("1d", False), ((2, 2), False), ("1d", True)])
+def test_layouts_same_bits(vs, tiling, periodic):
+    """Layouts are storage only: AoS and column fields give the SoA bits
+    (geometry.py:1-7), through the halo exchange of 2 or 4 ranks."""
     p = tl.PhysicsParams(tau=0.8, gy=-1e-4, Twall_top=0.6, Twall_bot=0.75)
-    kw = dict(Lx=24, Ly=20, Np=2, tiling="1d", steps=5, params=p, init="random",
-              init_kwargs={"seed": 9})
+    kw = dict(Lx=24, Ly=20, Np=2 if tiling == "1d" else 4, tiling=tiling, steps=5, params=p,
+              init="random", init_kwargs={"seed": 9}, walls=not periodic, periodic_y=periodic)
     a = tl.run(tl.SimConfig(layout="soa", **kw))
-    b = tl.run(tl.SimConfig(layout="aos", **kw))
-    assert np.array_equal(a.populations, b.populations)
+    for layout in ("aos", "column"):
+        b = tl.run(tl.SimConfig(layout=layout, **kw))
+        assert np.array_equal(a.populations, b.populations), layout
+
+
+def test_field_layout_conversion_round_trip(vs):
+    g = tl.LatticeGeometry(6, 5, 3, 3, 37)
+    f, _ = tl.allocate_field(g, vs)
+    f.pops.copy_(torch.randn(f.pops.shape, dtype=torch.float64, device=f.device))
+    for layout in (tl.AOS, tl.COLUMN):
+        c = f.converted(layout)
+        assert c.geom.layout == layout and torch.equal(c.pops, f.pops)
+        flat = c.flat
+        for (l, x, y) in [(0, 0, 0), (5, 2, 7), (36, 11, 10)]:
+            assert flat[tl.site_index(c.geom, l, x, y)].item() == f.pops[l, x, y].item()
+        assert torch.equal(c.converted(tl.SOA).data, f.data)
 
 
 def test_device_output_and_explicit_f0(vs):

@@ -55,6 +55,13 @@ def test_site_index_layouts():
     ga = tl.LatticeGeometry(4, 4, 3, 3, 9, tl.AOS)
     x, y = divmod(5, ga.NY)
     assert tl.site_index(ga, 2, x, y) == 5 * ga.Q + 2
+    gc = tl.LatticeGeometry(4, 4, 3, 3, 9, tl.COLUMN)
+    assert tl.site_index(gc, 0, 0, 1) == 1
+    assert tl.site_index(gc, 1, 0, 0) == gc.NY
+    assert tl.site_index(gc, 0, 1, 0) == gc.Q * gc.NY
+    offs = {tl.site_index(gc, l, x, y) for l in range(9) for x in range(gc.NX)
+            for y in range(gc.NY)}
+    assert offs == set(range(9 * gc.NX * gc.NY))
     with pytest.raises(tl.ContractViolation):
         tl.site_index(g, 9, 0, 0)
 

@@ -27,9 +27,10 @@ def main():
     ap.add_argument("--only", default="")
     ap.add_argument("--pad", type=int, default=0,
                     help="align: column pitch multiple of 16 doubles, y=Hy at a 128 B boundary")
+    ap.add_argument("--layout", default="column", choices=["column", "soa", "aos"])
     a = ap.parse_args()
     vs = tl.build_velocity_set("D2Q37")
-    g = tl.LatticeGeometry(a.Lx, a.Ly, 3, 3, 37)
+    g = tl.LatticeGeometry(a.Lx, a.Ly, 3, 3, 37, "soa" if a.pad else a.layout)
     prv, nxt = tl.allocate_field(g, vs)
     if a.pad:
         # same logical (Q, NX, NY) view over a padded, 128 B aligned allocation
