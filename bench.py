@@ -259,10 +259,15 @@ def gpu_arm(args, rank, world, local_rank):
 
     # warm-up (also sizes the clock pre-load identically on every rank: each
     # rank must run exactly the same number of ring steps)
-    tw = time.perf_counter()
     run_steps(args.warmup)
     w.synchronize()
-    step_s = (time.perf_counter() - tw) / args.warmup
+    # calibrate the step time after the warm-up (the first steps include
+    # one-time costs such as the NCCL ring's setup)
+    n_cal = 20
+    tw = time.perf_counter()
+    run_steps(n_cal, args.warmup)
+    w.synchronize()
+    step_s = (time.perf_counter() - tw) / n_cal
     if dist is not None:
         t = torch.tensor([step_s], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -274,7 +279,7 @@ def gpu_arm(args, rank, world, local_rank):
     # clocks: sample while a ~1 s untimed pre-load runs, then the timed steps
     sampler = ClockSampler(_gpu_index(local_rank))
     sampler.start()
-    s = args.warmup
+    s = args.warmup + n_cal
     for _ in range(0, n_pre, 10):
         run_steps(10, s)
         s += 10
