@@ -376,3 +376,70 @@ def test_pgm_bytes_match_reference(tmp_path):
     # a device (strided) view gives the same bytes
     t = torch.as_tensor(np.pad(g["T"], ((0, 0), (3, 3)))).cuda()[:, 3:-3]
     assert tio.pgm_bytes(t) == g["pgm"].tobytes()
+
+
+# ------------------------------------------------------ CUDA-graph replay --
+
+def _single_worker(vs, schedule, walls, arith="exact"):
+    p = tl.PhysicsParams(tau=0.8, gx=1e-6, gy=-1e-5, Twall_top=0.9 * vs.cs2,
+                         Twall_bot=1.1 * vs.cs2, arith=arith)
+    tile = tl.decompose(48, 40, 1, "1d", periodic_y=not walls)[0]
+    w = tl.RankWorker(tile, vs, p, tl.Fabric(1), schedule=schedule, walls=walls,
+                      periodic_y=not walls)
+    macro = tl.init.initial_macro("random", 48, 40, vs, seed=5)
+    w.load_block(tl.equilibrium(*[torch.as_tensor(m).cuda() for m in macro], vs))
+    return w
+
+
+@pytest.mark.parametrize("schedule,walls", [("overlapped", True), ("staged", True),
+                                            ("overlapped", False), ("staged", False)])
+def test_graph_replay_equals_step_loop(vs, schedule, walls):
+    """RankWorker.run_steps (CUDA graphs of 32 steps) gives the bits and the
+    per-step negatives of the plain step() loop, across graph boundaries and
+    for both buffer parities."""
+    a, b = _single_worker(vs, schedule, walls), _single_worker(vs, schedule, walls)
+    assert b.graphable()
+    for s in range(3 + 70 + 40):
+        a.step(s)
+    b.run_steps(0, 3)          # odd prefix: the graphs start on the other parity
+    b.run_steps(3, 69)         # 64 replayed + 5 plain -> even again
+    b.run_steps(72, 41)        # 32 replayed on the first parity + 9 plain
+    assert torch.equal(a.physical_block(), b.physical_block())
+    ma, mb = a.metrics, b.metrics
+    assert [m["negatives"] for m in ma] == [m["negatives"] for m in mb]
+    assert len(b._graphs) == 2
+
+
+def test_graph_replay_reports_failures_with_step(vs):
+    """A degenerate state is reported from inside a replayed graph with the
+    same step number as the step() loop (collect -> DegenerateStateError)."""
+    errs = []
+    for graphed in (False, True):
+        w = _single_worker(vs, "overlapped", True)
+        f = w.physical_block()
+        f[:, 20:24, 10:14] *= -1.0          # negative density in a patch
+        w.load_block(f)
+        if graphed:
+            w.run_steps(0, 64)
+        else:
+            for s in range(64):
+                w.step(s)
+        with pytest.raises(tl.DegenerateStateError) as e:
+            w.collect()
+        errs.append(str(e.value).split(":")[0])
+        x, y = e.value.sites[0]          # padded coordinates, first site flagged
+        assert 23 <= x < 27 and 13 <= y < 17
+    assert errs[0] == errs[1] == "rank 0 step 0"
+
+
+def test_run_uses_graphs_and_matches_multi_rank(vs):
+    p = tl.PhysicsParams(tau=0.8, gy=-1e-5, Twall_top=0.9 * vs.cs2, Twall_bot=1.1 * vs.cs2)
+    kw = dict(Lx=64, Ly=32, steps=100, params=p, init="rayleigh-taylor", snapshot_every=40)
+    one = tl.run(tl.SimConfig(Np=1, **kw))
+    two = tl.run(tl.SimConfig(Np=2, **kw))
+    assert np.array_equal(one.populations, two.populations)
+    assert [s for s, _ in one.snapshots] == [40, 80] == [s for s, _ in two.snapshots]
+    for (_, a), (_, b) in zip(one.snapshots, two.snapshots):
+        for name in ("rho", "ux", "uy", "T"):
+            assert np.array_equal(np.asarray(getattr(a, name)), np.asarray(getattr(b, name)))
+    assert len(one.metrics) == 100
