@@ -3,9 +3,10 @@
 Drop-in for the hot path of the reference package ``thermolb``
 (/root/reference/pkg/src/thermolb/__init__.py:3-26): the lattice, kernel,
 runtime and run APIs keep their names; the compute is hand-written sm_100a
-CUDA in libtlb.so (include/tlb.h), driven through ctypes.  The reference's
-analytic planner, CLI, IO and CPU micro-benchmarks are out of scope
-(SURVEY.md §2 rows 9-12).
+CUDA in libtlb.so (include/tlb.h), driven through ctypes.  The analytic
+planner (paper Eqs. 10-19) and the snapshot writers (``io``) are restated
+for the SURVEY §8(f) rows; the CLI and the CPU micro-benchmarks are out of
+scope.
 """
 
 from .errors import (AllocationError, ConfigurationError, ContractViolation,
@@ -17,6 +18,10 @@ from .geometry import (AOS, COLUMN, SOA, LatticeGeometry, MacroFields, Populatio
 from .kernels import (WALL_ROWS, PhysicsParams, apply_shift, bc, collide,
                       count_negative, equilibrium, moments, propagate,
                       propagate_collide_fused)
+from .planner import (BandwidthTable, CostModelInput, Prediction, brent_bound,
+                      comm_time_2d, optimal_grid, predict_1d, predict_1d_overlap,
+                      predict_2d, predict_2d_overlap, scaling_curve,
+                      surface_over_volume)
 from .runtime import (DistFabric, Fabric, RankWorker, TileAssignment,
                       boundary_bytes_per_site, decompose, face_plans)
 from .sim import RunResult, SimConfig, run
@@ -30,6 +35,9 @@ __all__ = [
     "RankWorker", "TileAssignment", "decompose", "face_plans",
     "boundary_bytes_per_site", "Fabric", "DistFabric",
     "RunResult", "SimConfig", "run",
+    "BandwidthTable", "CostModelInput", "Prediction", "brent_bound", "optimal_grid",
+    "predict_1d", "predict_1d_overlap", "predict_2d", "predict_2d_overlap",
+    "scaling_curve", "comm_time_2d", "surface_over_volume",
     "VelocitySet", "build_velocity_set",
     "ThermoLBError", "ConfigurationError", "ContractViolation", "DomainError",
     "DegenerateStateError", "AllocationError", "ProtocolError", "DeadlockError",

@@ -1,8 +1,8 @@
 """D2Q9 (and any non-specialised stencil) through the generic kernels, and
 the generic path cross-checked against the specialised D2Q37 kernels.
 
-Mirrors the reference's D2Q9 tests (tests/test_kernels.py:55-65, 172-183,
-224-229, 296-301, 334-353; test_runtime.py:58-61, 137-158) and compares
+Mirrors the reference's D2Q9 tests (tests/test_kernels.py:23-33, 140-151,
+192-197, 264-269, 302-321; test_runtime.py:58-61, 137-158) and compares
 with D2Q9 fixtures produced by the reference (tests/golden/d2q9.npz).
 """
 
@@ -69,25 +69,25 @@ def test_d2q9_run_bitwise(d2q9, g9, Np, schedule):
 
 
 def test_d2q9_reference_properties(d2q9):
-    # test_kernels.py:55-65 rest temperature, zero state rejected
+    # test_kernels.py:23-33 rest temperature, zero state rejected
     _, _, _, T = tl.moments(d2q9.w[:, None], d2q9)
     assert T[0] == pytest.approx(1 / 3, abs=1e-15)
     with pytest.raises(tl.DegenerateStateError):
         tl.moments(np.zeros((9, 1)), d2q9)
-    # test_kernels.py:172-176 momentum exact at order 2
+    # test_kernels.py:140-144 momentum exact at order 2
     f = tl.equilibrium(np.float64(1.0), 0.05, 0.0, np.float64(d2q9.cs2), d2q9)
     _, ux, uy, _ = tl.moments(f[:, None], d2q9)
     assert abs(ux[0] - 0.05) < 1e-12 and abs(uy[0]) < 1e-12
     with pytest.raises(tl.DomainError):
         tl.equilibrium(np.float64(-1.0), 0.0, 0.0, np.float64(0.3), d2q9)
-    # test_kernels.py:296-301 infinite-tau limit
+    # test_kernels.py:264-269 infinite-tau limit
     rng = np.random.default_rng(13)
     f = 0.2 + rng.random((9, 4))
     out = tl.collide(f, tl.PhysicsParams(tau=1e12), d2q9)
     assert np.allclose(out, f, rtol=1e-11)
-    # test_kernels.py:224-229 uniform state invariant under propagate
+    # test_kernels.py:192-197 uniform state invariant under propagate
     g, prv, nxt = field(d2q9, None, 8, 8)
-    prv.pops[...] = torch.as_tensor(d2q9.w)[:, None, None]
+    prv.pops[...] = torch.tensor(d2q9.w)[:, None, None]
     tl.propagate(prv, nxt, d2q9)
     assert torch.equal(nxt.pops[:, 3:11, 3:11], prv.pops[:, 3:11, 3:11])
 
