@@ -190,21 +190,27 @@ def reference_arm(args, rank, world):
     if rank != 0:
         return 0
     mlups, nthreads, done, sample = cpu_oracle_rate(None, steps=args.steps, warmup=args.warmup)
-    Lx = TILE_LX * world
+    if args.strong:
+        Lx, Ly = 8192, 16384
+        workload = f"D2Q37 RT {Lx}x{Ly} (strong scaling, {world} tiles)"
+    else:
+        Lx, Ly = args.Lx * world, args.Ly
+        workload = f"D2Q37 RT {Lx}x{Ly} (1-D X tiles of {args.Lx}x{args.Ly})"
     line = {
         "impl": "reference", "metric": METRIC, "value": round(mlups, 4), "unit": "MLUPS",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
+        # the workload's step at the sampled site rate
+        "ms_per_step": round(Lx * Ly / (mlups * 1e6) * 1e3, 3),
+        "higher_is_better": True, "scaling": "strong" if args.strong else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (Rayleigh-Taylor init)",
-        "config": {"workload": f"D2Q37 RT {Lx}x{TILE_LY} (1-D X tiles of {TILE_LX}x{TILE_LY})",
-                   "sample": sample},
+        "config": {"workload": workload, "sample": sample},
         "gflops_fp64": round(mlups * FLOP_SITE / 1e3, 3),
         "cpu_baseline": {"value": round(mlups, 4), "unit": "MLUPS", "cores": nthreads,
                          "kind": "port", "sample": sample},
         "e2e": {"value": round(mlups, 4), "unit": "MLUPS", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
     return 0
 
 
@@ -443,7 +449,7 @@ def gpu_arm(args, rank, world, local_rank):
             mlups_cpu, nthreads, done, sample = cpu_oracle_rate(args.cpu_seconds)
             out["cpu_baseline"] = {"value": round(mlups_cpu, 4), "unit": "MLUPS",
                                    "cores": nthreads, "kind": "port", "sample": sample}
-        print(json.dumps(out), flush=True)
+        emit(out)
     if dist is not None:
         dist.destroy_process_group()
     return 0
@@ -573,7 +579,26 @@ def split_kernels(w, tl, _lib, field_desc, torch):
     return res
 
 
+_RESULT_OUT = None
+
+
+def _reserve_stdout():
+    """Keep the process's stdout for the one JSON result line: native
+    libraries (NCCL's version banner, ...) and any stray print go to stderr."""
+    global _RESULT_OUT
+    if _RESULT_OUT is None:
+        sys.stdout.flush()
+        _RESULT_OUT = os.fdopen(os.dup(1), "w")
+        os.dup2(2, 1)
+
+
+def emit(obj):
+    out = _RESULT_OUT if _RESULT_OUT is not None else sys.stdout
+    print(json.dumps(obj), file=out, flush=True)
+
+
 def main():
+    _reserve_stdout()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=100)
