@@ -67,6 +67,8 @@ def main():
                                                       st.ptr, s),
         "fused_fast_plain": lambda: lib.tlb_fused(P, N, full, fa, 0, st.ptr, s),
         "fused_fast_step": lambda: lib.tlb_fused(P, N, full, fa, W | IMP, st.ptr, s),
+        "fused_fast_walls": lambda: lib.tlb_fused(P, N, full, fa, W, st.ptr, s),
+        "fused_fast_wrap": lambda: lib.tlb_fused(P, N, full, fa, _lib.F_WRAP_X, st.ptr, s),
     }
     def tuned(fn, key, val, default):
         def run():
@@ -80,9 +82,9 @@ def main():
         variants[f"fused_fast_step_minb{mb}"] = tuned(variants["fused_fast_step"], 1, mb, 4)
     sites = a.Lx * a.Ly
     out = {}
-    for name, fn in variants.items():
-        if a.only and name not in a.only.split(","):
-            continue
+    order = a.only.split(",") if a.only else list(variants)   # --only order, repeats allowed
+    for name in order:
+        fn = variants[name]
         ts = []
         for _ in range(a.reps + 1):
             e0 = torch.cuda.Event(enable_timing=True)
