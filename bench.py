@@ -576,6 +576,7 @@ def split_kernels(w, tl, _lib, field_desc, torch):
         res[name] = r
     w.collect(raise_errors=False)
     w._metrics.clear()
+    res["arith"] = "exact" if tp.arith == _lib.ARITH["exact"] else "fast"
     return res
 
 
