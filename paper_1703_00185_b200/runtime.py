@@ -329,7 +329,8 @@ class DistFabric:
 class _StepRecord:
     step: int
     status: object      # device slice (bytes) of the per-step status ring
-    events: tuple       # (t0, t1, t2, t3) CUDA events: comm / bulk / border
+    events: tuple       # (t0, t1, t2, t3) CUDA events: comm / bulk / border,
+                        # ("graph", e0, e1, G) for a replayed block, or None
 
 
 class RankWorker:
@@ -674,10 +675,19 @@ class RankWorker:
                 if len(self._records) + G > self._RING:
                     self.collect()
                 pos = len(self._records)
+                ev = None
+                if self.timing != "off":
+                    # one event pair per replay: every step of the block
+                    # reports the block's average step time as t_bulk
+                    ev = ("graph", torch.cuda.Event(enable_timing=True),
+                          torch.cuda.Event(enable_timing=True), G)
+                    ev[1].record(self.stream)
                 with torch.cuda.stream(self.stream):
                     graph.replay()
                     self._status_ring[pos:pos + G].copy_(self._gstatus)
-                self._records.extend(_StepRecord(s + j, self._status_ring[pos + j], None)
+                if ev is not None:
+                    ev[2].record(self.stream)
+                self._records.extend(_StepRecord(s + j, self._status_ring[pos + j], ev)
                                      for j in range(G))
                 s += G
         while s < end:
@@ -700,12 +710,19 @@ class RankWorker:
         saved = (self._records, self._count, self.timing)
         self._records, self.timing = [], "off"
         graph = torch.cuda.CUDAGraph()
+        # capture_begin/end directly: the torch.cuda.graph context manager
+        # also runs gc.collect() and empty_cache(), which cost tens of ms and
+        # force later allocations back to cudaMalloc
         try:
-            with torch.cuda.graph(graph, stream=self.stream, capture_error_mode="thread_local"):
-                self._gstatus.zero_()
-                for j in range(G):
-                    self._capture_slot = self._gstatus[j]
-                    self.step(j)
+            with torch.cuda.stream(self.stream):
+                graph.capture_begin(capture_error_mode="thread_local")
+                try:
+                    self._gstatus.zero_()
+                    for j in range(G):
+                        self._capture_slot = self._gstatus[j]
+                        self.step(j)
+                finally:
+                    graph.capture_end()
         finally:
             self._capture_slot = None
             self._records, self._count, self.timing = saved
@@ -893,6 +910,15 @@ class RankWorker:
             if rec.events is None:
                 nan = float("nan")
                 m = {"t_comm_nc": nan, "t_comm_c": nan, "t_bulk": nan, "t_border": nan}
+                m["negatives"] = int(s.negatives)
+                self._metrics.append(m)
+                if err is None and s.flags:
+                    err = (rec.step, s)
+                continue
+            if rec.events[0] == "graph":
+                _, g0, g1, nsteps = rec.events
+                m = {"t_comm_nc": 0.0, "t_comm_c": 0.0,
+                     "t_bulk": g0.elapsed_time(g1) * 1e-3 / nsteps, "t_border": 0.0}
                 m["negatives"] = int(s.negatives)
                 self._metrics.append(m)
                 if err is None and s.flags:

@@ -408,6 +408,9 @@ def test_graph_replay_equals_step_loop(vs, schedule, walls):
     ma, mb = a.metrics, b.metrics
     assert [m["negatives"] for m in ma] == [m["negatives"] for m in mb]
     assert len(b._graphs) == 2
+    # replayed steps report the block's average step time
+    replayed = [m["t_bulk"] for m in mb[3:3 + 64]]
+    assert all(np.isfinite(t) and t > 0 for t in replayed)
 
 
 def test_graph_replay_reports_failures_with_step(vs):
