@@ -404,7 +404,7 @@ def gpu_arm(args, rank, world, local_rank):
                  else " on 1 B200 (BASELINE configs[1])")),
                 "Lx": Lx, "Ly": Ly, "tiling": args.tiling, "schedule": args.schedule,
                 "arith": args.arith, "layout": args.layout, "tau": 0.8, "gy": -1e-5,
-                "exchange": args.exchange if world > 1 else None,
+                "exchange": w.exchange_mode if world > 1 else None,
                 "l2": "no flush: 2 x %.2f GB state per GPU >> 126 MB L2" % (
                     37 * (Lx_tile + 6) * (Ly_tile + 6) * 8 / 1e9)},
             "gflops_fp64": round(gflops, 2),
@@ -431,8 +431,9 @@ def gpu_arm(args, rank, world, local_rank):
                                  "reports TDP-based uJ/site)"}
                        if clocks and clocks.get("power_w_median") else None),
             "host_enqueue_ms_per_step": round(host_ms, 4),
-            "gpu_launches": args.steps * (1 if world == 1 else
-                                          (2 if args.exchange == "p2p" else 4)),
+            # our kernels per step: the fused step (N=1, or p2p: halo stores
+            # fused in); NCCL ring: pack, bulk, unpack, border (+ NCCL's own)
+            "gpu_launches": args.steps * (1 if w.exchange_mode in ("self", "p2p") else 4),
         }
         if split:
             out["split"] = split
@@ -614,7 +615,7 @@ def main():
     ap.add_argument("--schedule", default="overlapped", choices=["overlapped", "staged"])
     ap.add_argument("--layout", default="column", choices=["column", "soa", "aos"],
                     help="population storage order (results are identical)")
-    ap.add_argument("--exchange", default="nccl", choices=["nccl", "p2p"],
+    ap.add_argument("--exchange", default="auto", choices=["auto", "nccl", "p2p"],
                     help="N>1 X-halo transport: NCCL ring, or NVLink peer stores fused "
                          "into the step kernel")
     ap.add_argument("--Lx", type=int, default=TILE_LX, help="tile Lx per GPU")

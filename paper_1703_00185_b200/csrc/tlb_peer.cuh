@@ -3,11 +3,13 @@
 //
 // The border columns a rank computes at step s are exactly the halo its
 // neighbours read at step s+1.  So instead of pack -> NCCL -> unpack, the
-// threads that compute the 3 edge columns store their 37 outputs twice: into
-// the local nxt buffer and, through CUDA-IPC-mapped pointers, straight into
-// the neighbour's nxt buffer's halo columns (NVLink stores).  One launch per
-// step does bulk + borders + the transfer; a 1-thread signal kernel then
-// publishes "step s done" into both neighbours' mailboxes (st.release.sys).
+// threads that compute the 3 edge columns store their outputs twice: all 37
+// into the local nxt buffer and the face-crossing ones, through CUDA-IPC-mapped
+// pointers, straight into the neighbour's nxt buffer's halo columns (NVLink
+// stores).  One launch per step does bulk + borders + the transfer + the
+// signal: the last border block to finish publishes "step s done" into both
+// neighbours' mailboxes (st.release.sys); only border blocks read our halos
+// or write theirs, so the bulk need not finish first.
 //
 // Ordering (both directions reduce to one condition): at step s a rank's
 // border blocks may (a) read its own halo, written by the neighbours during
@@ -34,7 +36,8 @@ struct TlbPeer {
 
 struct PeerLaunch {
     double *rleft, *rright;        // neighbours' nxt buffers (same layout as ours)
-    unsigned long long *mb;        // our mailbox: [0] left done, [1] right done
+    unsigned long long *mb;        // our mailbox: [0] left done, [1] right done, [2] counter
+    unsigned long long *left_mb, *right_mb;  // the neighbours' mailboxes
     long long need;                // wait until both >= need
     int x_left0, x_right0, h;      // border bands [x_left0, +h), [x_right0, +h)
     int Lx;
@@ -125,26 +128,46 @@ __global__ void __launch_bounds__(128, 4)
         report(L.status, bits, x, y, L.step);
         store_all(f, L.dst, x, y);
         // the neighbour's halo: our left band -> left neighbour's right halo
-        // (column + Lx), our right band -> right neighbour's left halo (- Lx)
+        // (column + Lx), our right band -> right neighbour's left halo (- Lx).
+        // Only the populations its pull reads there cross the face: at halo
+        // depth d those with c_x <= -d (left neighbour) or c_x >= d (right
+        // neighbour) -- the face plan's 15 / 8 / 3 lines (runtime.py:94-107),
+        // 26 of the 111 values of the 3 columns.  No per-thread fence: the
+        // block barrier + one fence.sys before the border counter below
+        // order them before the release.
         const bool left_band = x < P.x_left0 + P.h;
+        const int d = left_band ? x - P.x_left0 + 1 : P.x_right0 + P.h - x;
         double *rb = left_band ? P.rleft : P.rright;
         const int rx = left_band ? x + P.Lx : x - P.Lx;
         double *q = rb + (long long)rx * L.dst.sx + (long long)y * L.dst.sy;
 #pragma unroll
-        for (int l = 0; l < Q; ++l) q[(long long)l * L.dst.sl] = f[l];
-        __threadfence_system();
+        for (int l = 0; l < Q; ++l) {
+            if (left_band ? CX(l) <= -d : CX(l) >= d) q[(long long)l * L.dst.sl] = f[l];
+        }
     }
     if (timed_out && threadIdx.x == 0) report(L.status, TLB_ST_PEER_TIMEOUT, x, y, L.step);
     if (L.flags & TLB_F_COUNT_NEG) count_neg(L.status, f, active);
-}
-
-// publish "step done" (value = peer step + 1) into both neighbours' mailboxes
-__global__ void k_peer_signal(unsigned long long *left_mb, unsigned long long *right_mb,
-                              unsigned long long value) {
-    __threadfence_system();
-    // we are our left neighbour's RIGHT neighbour and vice versa
-    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(left_mb + 1), "l"(value) : "memory");
-    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(right_mb), "l"(value) : "memory");
+    // The last border block to finish publishes "step done" to both
+    // neighbours: only border blocks read our halos and write theirs, so the
+    // bulk need not finish first.  Fence / counter / fence is the
+    // threadFenceReduction pattern at system scope: every border block's
+    // halo reads and remote stores precede its counter increment, and the
+    // last block's release stores follow all of them.
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        unsigned long long *ctr = P.mb + 2;
+        if (atomicAdd(ctr, 1ull) == (unsigned long long)(P.nbb - 1)) {
+            *ctr = 0;                      // next step (next kernel) starts from 0
+            __threadfence_system();
+            const unsigned long long v = (unsigned long long)P.need + 1;
+            // we are our left neighbour's RIGHT neighbour and vice versa
+            asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(P.left_mb + 1), "l"(v)
+                         : "memory");
+            asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(P.right_mb), "l"(v)
+                         : "memory");
+        }
+    }
 }
 
 extern "C" {
@@ -250,6 +273,8 @@ int tlb_peer_step(tlb_peer_t pr, const TlbField *prv, const TlbField *nxt, int p
     P.rleft = pr->left[parity];
     P.rright = pr->right[parity];
     P.mb = mailbox;
+    P.left_mb = pr->left_mb;
+    P.right_mb = pr->right_mb;
     P.need = peer_step;
     P.h = h;
     P.Lx = prv->Lx;
@@ -265,10 +290,7 @@ int tlb_peer_step(tlb_peer_t pr, const TlbField *prv, const TlbField *nxt, int p
         k_peer_step<true><<<nb, 128, 0, s>>>(L, P);
     else
         k_peer_step<false><<<nb, 128, 0, s>>>(L, P);
-    if ((e = launch_check("peer step"))) return e;
-    k_peer_signal<<<1, 1, 0, s>>>(pr->left_mb, pr->right_mb,
-                                  (unsigned long long)(peer_step + 1));
-    return launch_check("peer signal");
+    return launch_check("peer step");
 }
 
 }  // extern "C"

@@ -349,12 +349,12 @@ class RankWorker:
 
     def __init__(self, tile, vs, params, fabric=None, schedule="staged", walls=True,
                  layout="column", halo=DEFAULT_HALO, debug_poison=False, device=None,
-                 periodic_y=False, exchange="nccl", timing="sampled", timing_every=32):
+                 periodic_y=False, exchange="auto", timing="sampled", timing_every=32):
         torch = _lib.torch_cuda()
         if schedule not in ("staged", "overlapped"):
             raise ConfigurationError(f"unknown schedule {schedule!r}")
-        if exchange not in ("nccl", "p2p"):
-            raise ConfigurationError(f"unknown exchange {exchange!r} (nccl|p2p)")
+        if exchange not in ("auto", "nccl", "p2p"):
+            raise ConfigurationError(f"unknown exchange {exchange!r} (auto|nccl|p2p)")
         if timing not in ("sampled", "every", "off"):
             raise ConfigurationError(f"unknown timing {timing!r} (sampled|every|off)")
         self.timing, self.timing_every, self._count = timing, max(1, int(timing_every)), 0
@@ -410,13 +410,27 @@ class RankWorker:
             self._gstatus = None
             self._capture_slot = None
             self._peer = None
-            if (exchange == "p2p" and self._ring is not None and not self.y_exchange
-                    and not self.x_self and schedule == "overlapped"):
+            # NVLink peer stores fused into the step kernel (tlb_peer_step):
+            # 1-D ring, overlapped schedule, the specialised D2Q37 order-4
+            # kernels, tiles at least 7 columns wide.  "auto" takes it when
+            # it applies, else the NCCL ring; "p2p" insists.
+            order = params.eq_order if params.eq_order is not None else vs.eq_order
+            peer_ok = (self._ring is not None and not self.y_exchange and not self.x_self
+                       and schedule == "overlapped" and vs.Q == 37 and order == 4
+                       and tile.Lx >= 7)
+            if exchange == "p2p" and not peer_ok and self._ring is not None:
+                raise ConfigurationError(
+                    "exchange='p2p' needs a 1-D ring of D2Q37 order-4 tiles >= 7 columns "
+                    "wide with the overlapped schedule")
+            if exchange in ("auto", "p2p") and peer_ok:
                 self._setup_peer(fabric)
             # order the allocations' zero-fills before any work on our stream
             self.stream.wait_stream(torch.cuda.current_stream(self.device))
         self.plans = face_plans(vs, halo)
         self.tparams = _lib.params(params, vs)
+        self.exchange_mode = ("p2p" if self._peer is not None else
+                              "nccl" if self._ring is not None else
+                              "self" if self.x_self and not self.y_exchange else "fabric")
         self._records = []
         self._retained = []
         self._metrics = []
@@ -429,7 +443,9 @@ class RankWorker:
         import ctypes
         torch = _lib.torch_cuda()
         lib = _lib.load()
-        self.mailbox = torch.zeros(2, dtype=torch.int64, device=self.device)
+        # [0] left neighbour's step, [1] right neighbour's step (written by
+        # them), [2] this rank's border-block counter (tlb_peer_step)
+        self.mailbox = torch.zeros(4, dtype=torch.int64, device=self.device)
         torch.cuda.synchronize(self.device)
         mine = []
         for t in (self.prv.data, self.nxt.data, self.mailbox):

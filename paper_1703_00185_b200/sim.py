@@ -48,7 +48,8 @@ class SimConfig:
     recv_timeout: float = 60.0
     devices: "tuple | None" = None
     output: str = "host"
-    exchange: str = "nccl"   # one process per GPU: "nccl" ring or "p2p" (NVLink peer stores)
+    exchange: str = "auto"   # one process per GPU: "p2p" (NVLink peer stores fused into the
+                             # step kernel) where it applies, else the "nccl" ring
     timing: str = "sampled"  # per-step device timers: "sampled" (1 in 32), "every", "off"
 
     def __post_init__(self):

@@ -41,6 +41,7 @@ def main():
     tilings = ["1d", (1, world)] + ([(2, world // 2)] if world >= 4 else [])
     cases = [(t, sch, "nccl") for t in tilings for sch in ("overlapped", "staged")]
     cases.append(("1d", "overlapped", "p2p"))      # NVLink peer-store exchange
+    cases.append(("1d", "overlapped", "auto"))     # the default (p2p where it applies)
     ok = True
     for tiling, schedule, exchange in cases:
         for arith in (("exact", "fast") if exchange == "p2p" else ("exact",)):

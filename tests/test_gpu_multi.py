@@ -41,14 +41,16 @@ def test_torchrun_nccl_ring_bitwise(n):
     assert "DIST OK" in out.stdout
 
 
-def test_torchrun_stalled_neighbour_raises_deadlock():
-    """A rank whose ring neighbour stops stepping times out, aborts the NCCL
-    ring and raises DeadlockError instead of hanging (tests/dist_stall.py)."""
+@pytest.mark.parametrize("mode", ["nccl", "p2p"])
+def test_torchrun_stalled_neighbour_raises_deadlock(mode):
+    """A rank whose ring neighbour stops stepping raises DeadlockError instead
+    of hanging: NCCL ring -> host timeout + ring abort; peer stores -> the
+    kernel's bounded wait flags PEER_TIMEOUT (tests/dist_stall.py)."""
     if torch.cuda.device_count() < 2:
         pytest.skip("needs 2 GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            "--nproc-per-node=2", "--master-addr", "127.0.0.1",
-           "--master-port", str(_port()), os.path.join(ROOT, "tests", "dist_stall.py")]
+           "--master-port", str(_port()), os.path.join(ROOT, "tests", "dist_stall.py"), mode]
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=180, cwd=ROOT)
     print(out.stdout[-3000:], out.stderr[-3000:])
     assert out.returncode == 0
