@@ -6,9 +6,10 @@
 A "step" is one full time step (X-halo exchange + propagate + bc + collide,
 fused) of the whole lattice.  At N=1 the workload is BASELINE.json configs[1]
 (D2Q37 Rayleigh-Taylor 1920x2048 on one B200); at N>1 it is configs[2]
-(weak scaling, 1920x2048 per GPU, 1-D X tiling, overlapped halo exchange
-over NCCL), one process per GPU under torchrun.  Prints ONE JSON line on
-rank 0.
+(weak scaling, 1920x2048 per GPU, 1-D X tiling; the X halos travel as
+NVLink peer stores fused into the step kernel, or over an overlapped NCCL
+ring with --exchange nccl), one process per GPU under torchrun; --strong
+gives configs[3].  Prints ONE JSON line on rank 0.
 
 --impl reference times the reference algorithm on the host CPU (the C
 oracle restatement, all host threads) on a bounded sample of the workload.
@@ -399,7 +400,10 @@ def gpu_arm(args, rank, world, local_rank):
             "data": "synthetic (Rayleigh-Taylor initial state, reference init.py:45-64)",
             "config": {"workload": f"D2Q37 RT {Lx}x{Ly}" + (
                 f" ({'1-D X' if grid[1] == 1 else f'{grid[0]}x{grid[1]}'} tiles of "
-                f"{Lx_tile}x{Ly_tile}, overlapped halo exchange)" if world > 1 else
+                f"{Lx_tile}x{Ly_tile}, " + ("halo exchange fused into the step kernel as "
+                                            "NVLink peer stores)" if w.exchange_mode == "p2p"
+                                            else "overlapped NCCL halo exchange)")
+                if world > 1 else
                 (" on 1 B200 (BASELINE configs[3], strong-scaling base)" if args.strong
                  else " on 1 B200 (BASELINE configs[1])")),
                 "Lx": Lx, "Ly": Ly, "tiling": args.tiling, "schedule": args.schedule,
