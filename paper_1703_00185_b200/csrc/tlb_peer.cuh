@@ -36,7 +36,8 @@ struct TlbPeer {
 
 struct PeerLaunch {
     double *rleft, *rright;        // neighbours' nxt buffers (same layout as ours)
-    unsigned long long *mb;        // our mailbox: [0] left done, [1] right done, [2] counter
+    unsigned long long *mb;        // our mailbox: [0] left done, [1] right done, [2] counter,
+                                   // [3] sticky timeout flag
     unsigned long long *left_mb, *right_mb;  // the neighbours' mailboxes
     long long need;                // wait until both >= need
     int x_left0, x_right0, h;      // border bands [x_left0, +h), [x_right0, +h)
@@ -91,8 +92,11 @@ __global__ void __launch_bounds__(128, 4)
         const unsigned long long t0 = globaltimer();
         while (ld_acquire_sys(P.mb) < (unsigned long long)P.need ||
                ld_acquire_sys(P.mb + 1) < (unsigned long long)P.need) {
-            if (globaltimer() - t0 > TLB_PEER_TIMEOUT_NS) {
+            // mb[3]: a previous wait already timed out -> the neighbour is
+            // gone; later queued steps fail at once instead of 5 s each
+            if (ld_acquire_sys(P.mb + 3) || globaltimer() - t0 > TLB_PEER_TIMEOUT_NS) {
                 timed_out = 1;
+                atomicExch(P.mb + 3, 1ull);
                 break;
             }
             __nanosleep(256);

@@ -444,7 +444,8 @@ class RankWorker:
         torch = _lib.torch_cuda()
         lib = _lib.load()
         # [0] left neighbour's step, [1] right neighbour's step (written by
-        # them), [2] this rank's border-block counter (tlb_peer_step)
+        # them), [2] this rank's border-block counter, [3] sticky timeout
+        # flag (tlb_peer_step)
         self.mailbox = torch.zeros(4, dtype=torch.int64, device=self.device)
         torch.cuda.synchronize(self.device)
         mine = []

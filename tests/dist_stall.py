@@ -48,7 +48,7 @@ def main():
     w.synchronize()
     ok = True
     if rank == 0:
-        for s in range(2, 4):
+        for s in range(2, 2 + (2 if mode == "nccl" else 6)):   # p2p: later steps fail fast
             for phase in ("step_begin", "step_mid", "step_end"):
                 getattr(w, phase)(s)
         t0 = time.monotonic()
@@ -59,7 +59,9 @@ def main():
             print("rank 0: stalled step completed?!", flush=True)
         except tl.DeadlockError as exc:
             waited = time.monotonic() - t0
-            ok = exc.rank == 0 and 3.5 < waited < 30.0
+            # p2p: one 5 s bounded wait, then the sticky flag fails the
+            # other queued steps at once (5 waits would take 25 s)
+            ok = exc.rank == 0 and 3.5 < waited < (30.0 if mode == "nccl" else 12.0)
             print(f"rank 0 ({mode}): DeadlockError after {waited:.1f} s: {exc}", flush=True)
     flag = torch.tensor([int(ok)], device=dev)
     dist.all_reduce(flag, op=dist.ReduceOp.MIN)     # torch's own communicator
