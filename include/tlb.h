@@ -249,12 +249,14 @@ int tlb_ring_step(tlb_ring_t ring, const TlbField *prv, const TlbField *nxt,
                   tlb_stream_t stream);
 
 /* ---- X-halo exchange fused into the step over NVLink peer memory --------
- * (1-D ring, one process per GPU).  The border threads of a step store their
- * outputs both locally and into the neighbours' nxt halo columns through
- * CUDA-IPC mapped pointers; a 1-thread kernel then publishes the step into
- * the neighbours' mailboxes; border blocks of the next step wait for both
- * neighbours (bounded; TLB_ST_PEER_TIMEOUT on expiry).  Replaces pack ->
- * NCCL -> unpack of tlb_ring_step. */
+ * (1-D ring, one process per GPU; runtime.py:269-284 pbc_c + :355-400 step).
+ * One kernel per step: the border threads store their outputs locally and
+ * the face-plan lines (runtime.py:94-107) into the neighbours' nxt halo
+ * columns through CUDA-IPC mapped pointers; the last border block to finish
+ * publishes the step into the neighbours' mailboxes (st.release.sys); border
+ * blocks of the next step wait for both neighbours (bounded; sticky
+ * TLB_ST_PEER_TIMEOUT on expiry).  Replaces pack -> NCCL -> unpack of
+ * tlb_ring_step. */
 typedef struct TlbPeer *tlb_peer_t;
 /* 64-byte cudaIpcMemHandle of the allocation holding ptr, and ptr's offset */
 int tlb_ipc_handle(const void *ptr, char *out64, int64_t *offset);
@@ -264,7 +266,8 @@ int tlb_peer_create(int device, const char *handles, const int64_t *offsets,
                     tlb_peer_t *out);
 int tlb_peer_destroy(tlb_peer_t peer);
 /* One step.  nxt_index: 0 if nxt is buffer A, 1 if B.  mailbox: this rank's
- * 2 x u64 device mailbox ([0] left neighbour done, [1] right done; zeroed).
+ * 4 x u64 zeroed device mailbox ([0] left neighbour done, [1] right done,
+ * [2] border-block counter, [3] sticky timeout flag).
  * peer_step: 0, 1, 2, ... (border blocks wait for mailbox >= peer_step). */
 int tlb_peer_step(tlb_peer_t peer, const TlbField *prv, const TlbField *nxt,
                   int nxt_index, const TlbParams *p, int flags,
