@@ -1,47 +1,41 @@
 """B200-native D2Q37 thermal lattice Boltzmann step (arXiv 1703.00185).
 
-Drop-in for the hot path of the reference package ``thermolb``
-(/root/reference/pkg/src/thermolb/__init__.py:3-26): the lattice, kernel,
-runtime and run APIs keep their names; the compute is hand-written sm_100a
-CUDA in libtlb.so (include/tlb.h), driven through ctypes.  The analytic
-planner (paper Eqs. 10-19) and the snapshot writers (``io``) are restated
-for the SURVEY §8(f) rows; the CLI and the CPU micro-benchmarks are out of
-scope.
+A drop-in for the hot path of the reference package ``thermolb``: the
+public names of its lattice, kernel, runtime, run and planner modules are
+re-exported here unchanged, plus the B200 additions (column layout, NCCL /
+NVLink-peer ``DistFabric``, ``count_negative``, ``DeviceError``).  All
+compute runs in libtlb.so (hand-written sm_100a CUDA, C ABI in
+include/tlb.h) through ctypes; there is no CPU fallback.  Out of scope: the
+reference's CLI and its CPU micro-benchmarks.
 """
 
-from .errors import (AllocationError, ConfigurationError, ContractViolation,
-                     DeadlockError, DegenerateStateError, DeviceError,
-                     DomainError, ProtocolError, ThermoLBError,
-                     UnsupportedCaseError)
-from .geometry import (AOS, COLUMN, SOA, LatticeGeometry, MacroFields, PopulationField,
-                       allocate_field, site_index, swap_buffers)
-from .kernels import (WALL_ROWS, PhysicsParams, apply_shift, bc, collide,
-                      count_negative, equilibrium, moments, propagate,
-                      propagate_collide_fused)
-from .planner import (BandwidthTable, CostModelInput, Prediction, brent_bound,
-                      comm_time_2d, optimal_grid, predict_1d, predict_1d_overlap,
-                      predict_2d, predict_2d_overlap, scaling_curve,
-                      surface_over_volume)
-from .runtime import (DistFabric, Fabric, RankWorker, TileAssignment,
-                      boundary_bytes_per_site, decompose, face_plans)
-from .sim import RunResult, SimConfig, run
-from .velocity_set import VelocitySet, build_velocity_set
+from importlib import import_module
 
-__all__ = [
-    "AOS", "COLUMN", "SOA", "LatticeGeometry", "MacroFields", "PopulationField",
-    "allocate_field", "site_index", "swap_buffers",
-    "PhysicsParams", "apply_shift", "bc", "collide", "equilibrium", "moments",
-    "propagate", "propagate_collide_fused", "count_negative", "WALL_ROWS",
-    "RankWorker", "TileAssignment", "decompose", "face_plans",
-    "boundary_bytes_per_site", "Fabric", "DistFabric",
-    "RunResult", "SimConfig", "run",
-    "BandwidthTable", "CostModelInput", "Prediction", "brent_bound", "optimal_grid",
-    "predict_1d", "predict_1d_overlap", "predict_2d", "predict_2d_overlap",
-    "scaling_curve", "comm_time_2d", "surface_over_volume",
-    "VelocitySet", "build_velocity_set",
-    "ThermoLBError", "ConfigurationError", "ContractViolation", "DomainError",
-    "DegenerateStateError", "AllocationError", "ProtocolError", "DeadlockError",
-    "UnsupportedCaseError", "DeviceError",
-]
+# module -> public names re-exported at package level
+_PUBLIC = {
+    "errors": "ThermoLBError ConfigurationError ContractViolation DomainError "
+              "DegenerateStateError AllocationError ProtocolError DeadlockError "
+              "UnsupportedCaseError DeviceError",
+    "velocity_set": "VelocitySet build_velocity_set",
+    "geometry": "SOA AOS COLUMN LatticeGeometry PopulationField MacroFields "
+                "allocate_field swap_buffers site_index",
+    "kernels": "PhysicsParams moments equilibrium apply_shift collide propagate bc "
+               "propagate_collide_fused count_negative WALL_ROWS",
+    "runtime": "TileAssignment decompose face_plans boundary_bytes_per_site "
+               "RankWorker Fabric DistFabric",
+    "sim": "SimConfig RunResult run",
+    "planner": "BandwidthTable CostModelInput Prediction surface_over_volume "
+               "comm_time_2d optimal_grid predict_1d predict_2d predict_1d_overlap "
+               "predict_2d_overlap brent_bound scaling_curve",
+}
 
+__all__ = []
+for _mod, _names in _PUBLIC.items():
+    _m = import_module(f".{_mod}", __name__)
+    for _n in _names.split():
+        globals()[_n] = getattr(_m, _n)
+        __all__.append(_n)
+from . import init, io  # noqa: E402  (submodules: presets, snapshot writers)
+
+del _mod, _names, _m, _n
 __version__ = "0.1.0"

@@ -1,4 +1,4 @@
-"""Snapshot output and config loading (io.py of the reference, io.py:13-80).
+"""Snapshot writers, tables and YAML configs (reference io.py:13-80).
 
 The observables come off the device already reduced: ``write_pgm`` of a
 device field runs the min/max + 8-bit quantisation on the GPU
@@ -8,7 +8,6 @@ same kernel after an upload.  Byte-identical to the reference's image
 """
 
 import csv
-import os
 
 import numpy as np
 
@@ -34,56 +33,65 @@ def pgm_bytes(values):
 
 
 def write_pgm(path, values):
-    """8-bit binary PGM (P5) of a (Lx, Ly) scalar field, min-max normalised;
-    image rows run top to bottom (decreasing lattice y) (io.py:13-24)."""
-    data = pgm_bytes(values)
+    """P5 snapshot of a (Lx, Ly) field: min-max scaled to 0..255, first
+    image row = largest y (reference io.py:13-24, same bytes)."""
     with open(path, "wb") as fh:
-        fh.write(data)
+        fh.write(pgm_bytes(values))
 
 
 def _host(a):
     return a.cpu().numpy() if hasattr(a, "cpu") else np.asarray(a)
 
 
-def write_macro_csv(path, macro: MacroFields):
-    """Row-major CSV of the macroscopic fields with a labelled header
-    (io.py:27-40)."""
-    rho, ux, uy, T = (_host(a) for a in (macro.rho, macro.ux, macro.uy, macro.T))
-    Lx, Ly = rho.shape
+_MACRO_HEADER = ("x [site]", "y [site]", "rho [lattice]", "ux [lattice]",
+                 "uy [lattice]", "T [lattice]")
+_METRIC_HEADER = ("step", "rank", "t_comm_nc [s]", "t_comm_c [s]", "t_bulk [s]",
+                  "t_border [s]", "negative_populations [count]")
+
+
+def _csv(path, header, rows):
     with open(path, "w", newline="") as fh:
-        w = csv.writer(fh)
-        w.writerow(["x [site]", "y [site]", "rho [lattice]", "ux [lattice]",
-                    "uy [lattice]", "T [lattice]"])
-        for x in range(Lx):
-            for y in range(Ly):
-                w.writerow([x, y, repr(float(rho[x, y])), repr(float(ux[x, y])),
-                            repr(float(uy[x, y])), repr(float(T[x, y]))])
+        out = csv.writer(fh)
+        out.writerow(list(header))
+        out.writerows(rows)
+
+
+def write_macro_csv(path, macro: MacroFields):
+    """One CSV row per site, x-major, values as Python float reprs (the
+    reference's format, io.py:27-40); device fields are copied back once."""
+    cols = [_host(getattr(macro, k)) for k in ("rho", "ux", "uy", "T")]
+    nx, ny = cols[0].shape
+
+    def rows():
+        for x in range(nx):
+            for y in range(ny):
+                yield [x, y] + [repr(float(c[x, y])) for c in cols]
+
+    _csv(path, _MACRO_HEADER, rows())
 
 
 def write_table(path, header, rows):
-    """io.py:43-47."""
-    with open(path, "w", newline="") as fh:
-        w = csv.writer(fh)
-        w.writerow(header)
-        w.writerows(rows)
+    """Plain CSV: a header row then the rows (reference io.py:43-47)."""
+    _csv(path, header, rows)
 
 
 def write_metrics(path, metrics):
     """Per-(step, rank) metrics table in the reference CLI's format
     (cli.py:69-75)."""
-    write_table(path, ["step", "rank", "t_comm_nc [s]", "t_comm_c [s]", "t_bulk [s]",
-                       "t_border [s]", "negative_populations [count]"],
-                [[m["step"], m["rank"], repr(m["t_comm_nc"]), repr(m["t_comm_c"]),
-                  repr(m["t_bulk"]), repr(m["t_border"]), m["negatives"]] for m in metrics])
+    times = ("t_comm_nc", "t_comm_c", "t_bulk", "t_border")
+    _csv(path, _METRIC_HEADER,
+         ([m["step"], m["rank"]] + [repr(m[k]) for k in times] + [m["negatives"]]
+          for m in metrics))
 
 
 def load_config(path):
-    """YAML run configuration: a mapping of explicit keys (io.py:72-80)."""
+    """A YAML mapping of run settings (reference io.py:72-80)."""
     import yaml
-    if not os.path.exists(path):
-        raise ConfigurationError(f"config file {path!r} not found")
-    with open(path) as fh:
-        data = yaml.safe_load(fh)
-    if not isinstance(data, dict):
-        raise ConfigurationError(f"{path}: expected a key/value mapping")
-    return data
+    try:
+        with open(path) as fh:
+            cfg = yaml.safe_load(fh)
+    except FileNotFoundError:
+        raise ConfigurationError(f"config file {path!r} not found") from None
+    if isinstance(cfg, dict):
+        return cfg
+    raise ConfigurationError(f"{path}: expected a key/value mapping")

@@ -41,17 +41,23 @@ def orc(stencil):
 
 
 def periodic_fill(pops, H=3):
-    """Wrap halos periodically in both directions (reference
-    tests/conftest.py:17-27), on a (Q, NX, NY) array (numpy or torch)."""
-    Q, NX, NY = pops.shape
-    Lx, Ly = NX - 2 * H, NY - 2 * H
-    pops[:, :H, :] = pops[:, Lx:Lx + H, :]
-    pops[:, H + Lx:, :] = pops[:, H:2 * H, :]
-    pops[:, :, :H] = pops[:, :, Ly:Ly + H]
-    pops[:, :, H + Ly:] = pops[:, :, H:2 * H]
+    """Fill the H-wide halo frame of a (Q, NX, NY) array (numpy or torch)
+    from the opposite physical edges, corners included -- the periodic
+    wrap of the reference's tests/conftest.py:17-27.  X first, then Y over
+    full columns, so corners come out right."""
+    NX, NY = pops.shape[1], pops.shape[2]
+    for axis, n in ((1, NX), (2, NY)):
+        L = n - 2 * H
+        lo_halo, hi_src = slice(0, H), slice(L, L + H)
+        hi_halo, lo_src = slice(H + L, n), slice(H, 2 * H)
+        for dst, src in ((lo_halo, hi_src), (hi_halo, lo_src)):
+            idx_d = [slice(None)] * 3
+            idx_s = [slice(None)] * 3
+            idx_d[axis], idx_s[axis] = dst, src
+            pops[tuple(idx_d)] = pops[tuple(idx_s)]
 
 
 def random_state(NX, NY, seed=0, lo=0.5, Q=37):
-    """Reference tests/conftest.py:30-32."""
-    rng = np.random.default_rng(seed)
-    return lo + rng.random((Q, NX, NY))
+    """lo + U[0, 1) of shape (Q, NX, NY): the same draws as the reference's
+    tests/conftest.py:30-32 for a given seed."""
+    return lo + np.random.default_rng(seed).random((Q, NX, NY))
