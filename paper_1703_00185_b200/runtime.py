@@ -33,7 +33,7 @@ import numpy as np
 
 from . import _lib
 from .errors import (ConfigurationError, DeadlockError, DegenerateStateError,
-                     DomainError, ProtocolError, ThermoLBError)
+                     DeviceError, DomainError, ProtocolError, ThermoLBError)
 from .geometry import LatticeGeometry, allocate_field, swap_buffers
 from .kernels import WALL_ROWS, field_desc
 from .velocity_set import VelocitySet
@@ -423,7 +423,7 @@ class RankWorker:
                     "exchange='p2p' needs a 1-D ring of D2Q37 order-4 tiles >= 7 columns "
                     "wide with the overlapped schedule")
             if exchange in ("auto", "p2p") and peer_ok:
-                self._setup_peer(fabric)
+                self._setup_peer(fabric, strict=exchange == "p2p")
             # order the allocations' zero-fills before any work on our stream
             self.stream.wait_stream(torch.cuda.current_stream(self.device))
         self.plans = face_plans(vs, halo)
@@ -437,10 +437,15 @@ class RankWorker:
         self.snapshots = []
         self._primed = False
 
-    def _setup_peer(self, fabric):
+    def _setup_peer(self, fabric, strict=False):
         """Map the ring neighbours' field buffers and mailboxes (CUDA IPC over
-        NVLink) for the fused peer-memory step (csrc/tlb_peer.cuh)."""
+        NVLink) for the fused peer-memory step (csrc/tlb_peer.cuh).
+
+        Collective: if any rank cannot export or open the IPC mappings, every
+        rank falls back to the NCCL ring together (or, with strict=True,
+        i.e. exchange="p2p", every rank raises DeviceError)."""
         import ctypes
+        import warnings
         torch = _lib.torch_cuda()
         lib = _lib.load()
         # [0] left neighbour's step, [1] right neighbour's step (written by
@@ -448,21 +453,47 @@ class RankWorker:
         # flag (tlb_peer_step)
         self.mailbox = torch.zeros(4, dtype=torch.int64, device=self.device)
         torch.cuda.synchronize(self.device)
-        mine = []
-        for t in (self.prv.data, self.nxt.data, self.mailbox):
-            h = ctypes.create_string_buffer(64)
-            off = ctypes.c_int64(0)
-            _lib.check(lib.tlb_ipc_handle(t.data_ptr(), h, ctypes.byref(off)), "ipc handle")
-            mine.append((bytes(h.raw), int(off.value)))
+
+        def agree(ok, why):
+            votes = [None] * fabric.Np
+            fabric.dist.all_gather_object(votes, (ok, why), group=fabric.group)
+            bad = [f"rank {r}: {w}" for r, (o, w) in enumerate(votes) if not o]
+            if bad and strict:
+                raise DeviceError("peer-store exchange unavailable: " + "; ".join(bad))
+            if bad:
+                warnings.warn("peer-store exchange unavailable, using the NCCL ring: "
+                              + "; ".join(bad))
+            return not bad
+
+        mine, why = [], ""
+        try:
+            for t in (self.prv.data, self.nxt.data, self.mailbox):
+                h = ctypes.create_string_buffer(64)
+                off = ctypes.c_int64(0)
+                _lib.check(lib.tlb_ipc_handle(t.data_ptr(), h, ctypes.byref(off)),
+                           "ipc handle")
+                mine.append((bytes(h.raw), int(off.value)))
+        except ThermoLBError as exc:
+            mine, why = None, str(exc)
         allinfo = [None] * fabric.Np
         fabric.dist.all_gather_object(allinfo, mine, group=fabric.group)
+        if not agree(mine is not None, why):
+            return
         nb = self.tile.neighbors
         order = allinfo[nb["left"]] + allinfo[nb["right"]]
         handles = b"".join(h for h, _ in order)
         offs = (ctypes.c_int64 * 6)(*[o for _, o in order])
         hp = ctypes.c_void_p()
-        _lib.check(lib.tlb_peer_create(self.device.index, handles, offs, ctypes.byref(hp)),
-                   "peer create")
+        try:
+            _lib.check(lib.tlb_peer_create(self.device.index, handles, offs, ctypes.byref(hp)),
+                       "peer create")
+            ok, why = True, ""
+        except ThermoLBError as exc:
+            ok, why = False, str(exc)
+        if not agree(ok, why):
+            if ok:
+                lib.tlb_peer_destroy(hp)
+            return
         self._peer = hp
         self._bufA = self.prv.data.data_ptr()
         self._peer_step = 0
