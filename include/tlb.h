@@ -249,7 +249,8 @@ int tlb_ring_step(tlb_ring_t ring, const TlbField *prv, const TlbField *nxt,
                   tlb_stream_t stream);
 
 /* ---- X-halo exchange fused into the step over NVLink peer memory --------
- * (1-D ring, one process per GPU; runtime.py:269-284 pbc_c + :355-400 step).
+ * (1-D ring or 2-D grid, one process per GPU; runtime.py:226-284 pbc_nc /
+ * pbc_c + :355-400 step).
  * One kernel per step: the border threads store their outputs locally and
  * the face-plan lines (runtime.py:94-107) into the neighbours' nxt halo
  * columns through CUDA-IPC mapped pointers; the last border block to finish
@@ -264,10 +265,15 @@ int tlb_ipc_handle(const void *ptr, char *out64, int64_t *offset);
  * right mailbox; A = the buffer that is prv at even peer steps. */
 int tlb_peer_create(int device, const char *handles, const int64_t *offsets,
                     tlb_peer_t *out);
+/* 2-D grid: 8 directions d = left, right, down, up, down-left, down-right,
+ * up-left, up-right; handles/offsets hold (A, B, mailbox) per direction
+ * (24 each), present[8] marks the exchanged directions (others ignored). */
+int tlb_peer_create2(int device, const char *handles, const int64_t *offsets,
+                     const int *present, tlb_peer_t *out);
 int tlb_peer_destroy(tlb_peer_t peer);
 /* One step.  nxt_index: 0 if nxt is buffer A, 1 if B.  mailbox: this rank's
- * 4 x u64 zeroed device mailbox ([0] left neighbour done, [1] right done,
- * [2] border-block counter, [3] sticky timeout flag).
+ * zeroed device mailbox of >= 10 u64 ([0..7] step published by the
+ * neighbour in direction d, [8] border-block counter, [9] sticky timeout).
  * peer_step: 0, 1, 2, ... (border blocks wait for mailbox >= peer_step). */
 int tlb_peer_step(tlb_peer_t peer, const TlbField *prv, const TlbField *nxt,
                   int nxt_index, const TlbParams *p, int flags,

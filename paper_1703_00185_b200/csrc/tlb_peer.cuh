@@ -1,50 +1,67 @@
-// tlb_peer.cuh -- the X-halo exchange fused into the step kernel over
-// NVLink peer memory (1-D ring, one process per GPU).
+// tlb_peer.cuh -- the halo exchange fused into the step kernel over NVLink
+// peer memory (one process per GPU; 1-D ring or 2-D rank grid).
 //
-// The border columns a rank computes at step s are exactly the halo its
+// The border sites a rank computes at step s are exactly the halo its
 // neighbours read at step s+1.  So instead of pack -> NCCL -> unpack, the
-// threads that compute the 3 edge columns store their outputs twice: all 37
-// into the local nxt buffer and the face-crossing ones, through CUDA-IPC-mapped
-// pointers, straight into the neighbour's nxt buffer's halo columns (NVLink
-// stores).  One launch per step does bulk + borders + the transfer + the
-// signal: the last border block to finish publishes "step s done" into both
-// neighbours' mailboxes (st.release.sys); only border blocks read our halos
-// or write theirs, so the bulk need not finish first.
+// threads that compute the 3-wide border bands store their outputs twice:
+// all 37 into the local nxt buffer and the face-crossing ones, through
+// CUDA-IPC-mapped pointers, straight into the neighbours' nxt halos (NVLink
+// stores).  On a 2-D grid a corner site also stores into the diagonal
+// neighbour's corner halo, so no Y-before-X ordering is needed: NVSwitch
+// reaches all 8 neighbours in one hop.  One launch per step does bulk +
+// borders + transfer + signal: the last border block to finish publishes
+// "step s done" into every neighbour's mailbox (st.release.sys); only border
+// blocks read our halos or write theirs, so the bulk need not finish first.
 //
-// Ordering (both directions reduce to one condition): at step s a rank's
-// border blocks may (a) read its own halo, written by the neighbours during
-// their step s-1, and (b) overwrite the neighbours' nxt halo, which the
-// neighbours last read during their step s-1.  Border blocks therefore wait
-// until both neighbours have published step s-1 (mailbox >= s).  Bulk blocks
-// never wait.  Border blocks get the LOWEST block indices: in lock step the
-// neighbours publish within microseconds, and a border block that waits
-// holds one CTA slot while the bulk fills the rest of the GPU (placing them
-// last instead leaves their latency as a tail: measured slower).  The wait
-// is bounded (TLB_PEER_TIMEOUT_NS) and reports TLB_ST_PEER_TIMEOUT instead of
-// hanging.
+// Ordering: at step s a rank's border blocks may (a) read its own halos,
+// written by the neighbours during their step s-1, and (b) overwrite the
+// neighbours' nxt halos, which the neighbours last read during their step
+// s-1.  Border blocks therefore wait until every neighbour has published
+// step s-1 (mailbox >= s).  Bulk blocks never wait.  Border blocks get the
+// LOWEST block indices: in lock step the neighbours publish within
+// microseconds, and a waiting border block holds one CTA slot while the bulk
+// fills the rest of the GPU (placing them last leaves their latency as a
+// tail: measured slower).  The wait is bounded (TLB_PEER_TIMEOUT_NS); an
+// expiry flags TLB_ST_PEER_TIMEOUT and is sticky (later queued steps fail at
+// once instead of waiting again).
 #pragma once
 
 #define TLB_PEER_TIMEOUT_NS 5000000000ull
 
+// directions d = (dx, dy): 0 left, 1 right, 2 down, 3 up, 4 down-left,
+// 5 down-right, 6 up-left, 7 up-right; POPP(d) is the reverse direction
+__host__ __device__ constexpr int PDX(int d) {
+    return (d == 0 || d == 4 || d == 6) ? -1 : (d == 1 || d == 5 || d == 7) ? 1 : 0;
+}
+__host__ __device__ constexpr int PDY(int d) {
+    return (d == 2 || d == 4 || d == 5) ? -1 : (d == 3 || d == 6 || d == 7) ? 1 : 0;
+}
+__host__ __device__ constexpr int POPP(int d) { return d < 4 ? (d ^ 1) : 11 - d; }
+
+// mailbox layout (u64): [0..7] step published by the neighbour in direction
+// d, [8] border-block counter, [9] sticky timeout flag
+#define TLB_MB_COUNTER 8
+#define TLB_MB_STICKY 9
+
 struct TlbPeer {
     int device = 0;
-    // neighbours' buffers A/B (A = the one that is prv at even peer steps)
-    double *left[2] = {nullptr, nullptr}, *right[2] = {nullptr, nullptr};
-    unsigned long long *left_mb = nullptr, *right_mb = nullptr;  // their mailboxes
-    void *opened[6] = {};
+    int present[8] = {};
+    double *buf[8][2] = {};              // neighbours' buffers A/B
+    unsigned long long *mb[8] = {};      // neighbours' mailboxes
+    void *opened[24] = {};
 };
 
 struct PeerLaunch {
-    double *rleft, *rright;        // neighbours' nxt buffers (same layout as ours)
-    unsigned long long *mb;        // our mailbox: [0] left done, [1] right done, [2] counter,
-                                   // [3] sticky timeout flag
-    unsigned long long *left_mb, *right_mb;  // the neighbours' mailboxes
-    long long need;                // wait until both >= need
-    int x_left0, x_right0, h;      // border bands [x_left0, +h), [x_right0, +h)
-    int Lx;
-    unsigned nbb;                  // border blocks (the last ones)
-    Rect br[2];
-    unsigned br_end[2];
+    double *nb[8];                 // neighbours' nxt buffers (same layout as ours)
+    unsigned long long *nbmb[8];   // neighbours' mailboxes
+    unsigned long long *mb;        // ours
+    int present;                   // bit d: a neighbour in direction d
+    long long need;                // wait until every present mailbox slot >= need
+    int xb, yb_lo, yb_hi;          // exchanged sides: X (both), bottom, top
+    int Hx, Hy, Lx, Ly;
+    unsigned nbb;                  // border blocks (the first ones)
+    Rect br[4];                    // left, right (full height), bottom, top (in between)
+    unsigned br_end[4];
 };
 
 __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
@@ -57,6 +74,25 @@ __device__ __forceinline__ unsigned long long globaltimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     return t;
+}
+
+// Store the populations of f that cross into direction d: at halo depth
+// (ddx, ddy) those with c_x <= -ddx (left) / >= ddx (right) and c_y <= -ddy
+// (down) / >= ddy (up) -- the face plans of runtime.py:94-107 and, at the
+// corners, their intersections.  Our site (x, y) is (x - dx Lx, y - dy Ly)
+// in the neighbour's frame.
+template <int d>
+__device__ __forceinline__ void peer_put(const PeerLaunch &P, const Fld &D, const double (&f)[Q],
+                                         int x, int y, int ddx, int ddy) {
+    if (!(P.present >> d & 1)) return;
+    double *q = P.nb[d] + (long long)(x - PDX(d) * P.Lx) * D.sx +
+                (long long)(y - PDY(d) * P.Ly) * D.sy;
+#pragma unroll
+    for (int l = 0; l < Q; ++l) {
+        const bool okx = PDX(d) < 0 ? CX(l) <= -ddx : PDX(d) > 0 ? CX(l) >= ddx : true;
+        const bool oky = PDY(d) < 0 ? CY(l) <= -ddy : PDY(d) > 0 ? CY(l) >= ddy : true;
+        if (okx && oky) q[(long long)l * D.sl] = f[l];
+    }
 }
 
 template <bool EXACT>
@@ -85,34 +121,38 @@ __global__ void __launch_bounds__(128, 4)
         }
         return;
     }
-    // ---- border blocks: wait for both neighbours' step s-1 ----
+    // ---- border blocks: wait for every neighbour's step s-1 ----
     __shared__ int timed_out;
     if (threadIdx.x == 0) {
-        timed_out = 0;
+        int late = 0;
         const unsigned long long t0 = globaltimer();
-        while (ld_acquire_sys(P.mb) < (unsigned long long)P.need ||
-               ld_acquire_sys(P.mb + 1) < (unsigned long long)P.need) {
-            // mb[3]: a previous wait already timed out -> the neighbour is
-            // gone; later queued steps fail at once instead of 5 s each
-            if (ld_acquire_sys(P.mb + 3) || globaltimer() - t0 > TLB_PEER_TIMEOUT_NS) {
-                timed_out = 1;
-                atomicExch(P.mb + 3, 1ull);
-                break;
+        for (int d = 0; d < 8 && !late; ++d) {
+            if (!(P.present >> d & 1)) continue;
+            while (ld_acquire_sys(P.mb + d) < (unsigned long long)P.need) {
+                // a previous wait already timed out -> a neighbour is gone;
+                // later queued steps fail at once instead of 5 s each
+                if (ld_acquire_sys(P.mb + TLB_MB_STICKY) ||
+                    globaltimer() - t0 > TLB_PEER_TIMEOUT_NS) {
+                    late = 1;
+                    atomicExch(P.mb + TLB_MB_STICKY, 1ull);
+                    break;
+                }
+                __nanosleep(256);
             }
-            __nanosleep(256);
         }
+        timed_out = late;
     }
     __syncthreads();
-    const unsigned total = P.br_end[1];
+    const unsigned total = P.br_end[3];
     const unsigned i = blockIdx.x * blockDim.x + threadIdx.x;
     const bool active = i < total && !timed_out;
     const unsigned ii = i < total ? i : total - 1;
-    const int r = ii < P.br_end[0] ? 0 : 1;
-    const unsigned loc = ii - (r ? P.br_end[0] : 0u);
+    const int r = ii < P.br_end[0] ? 0 : ii < P.br_end[1] ? 1 : ii < P.br_end[2] ? 2 : 3;
+    const unsigned loc = ii - (r ? P.br_end[r - 1] : 0u);
     const Rect &R = P.br[r];
     const int x = R.x0 + (int)(loc / R.ny), y = R.y0 + (int)(loc % R.ny);
     double f[Q];
-    const bool implicit = (L.flags & (TLB_F_WRAP_Y | TLB_F_CLAMP_Y)) != 0;
+    const bool implicit = (L.flags & (TLB_F_WRAP_X | TLB_F_WRAP_Y | TLB_F_CLAMP_Y)) != 0;
     load_all(f, L.src, x, y, true, implicit, L.flags);
     unsigned bits = 0;
     {
@@ -131,45 +171,44 @@ __global__ void __launch_bounds__(128, 4)
     if (active) {
         report(L.status, bits, x, y, L.step);
         store_all(f, L.dst, x, y);
-        // the neighbour's halo: our left band -> left neighbour's right halo
-        // (column + Lx), our right band -> right neighbour's left halo (- Lx).
-        // Only the populations its pull reads there cross the face: at halo
-        // depth d those with c_x <= -d (left neighbour) or c_x >= d (right
-        // neighbour) -- the face plan's 15 / 8 / 3 lines (runtime.py:94-107),
-        // 26 of the 111 values of the 3 columns.  No per-thread fence: the
-        // block barrier + one fence.sys before the border counter below
-        // order them before the release.
-        const bool left_band = x < P.x_left0 + P.h;
-        const int d = left_band ? x - P.x_left0 + 1 : P.x_right0 + P.h - x;
-        double *rb = left_band ? P.rleft : P.rright;
-        const int rx = left_band ? x + P.Lx : x - P.Lx;
-        double *q = rb + (long long)rx * L.dst.sx + (long long)y * L.dst.sy;
-#pragma unroll
-        for (int l = 0; l < Q; ++l) {
-            if (left_band ? CX(l) <= -d : CX(l) >= d) q[(long long)l * L.dst.sl] = f[l];
-        }
+        // depth of this site inside each exchanged band (0 = not in it).  No
+        // per-thread fence: the block barrier + one fence.sys before the
+        // border counter below order these stores before the release.
+        const int h = TLB_WALL_ROWS;
+        const int dl = P.xb && x < P.Hx + h ? x - P.Hx + 1 : 0;
+        const int dr = P.xb && x >= P.Hx + P.Lx - h ? P.Hx + P.Lx - x : 0;
+        const int db = P.yb_lo && y < P.Hy + h ? y - P.Hy + 1 : 0;
+        const int dt = P.yb_hi && y >= P.Hy + P.Ly - h ? P.Hy + P.Ly - y : 0;
+        if (dl) peer_put<0>(P, L.dst, f, x, y, dl, 0);
+        if (dr) peer_put<1>(P, L.dst, f, x, y, dr, 0);
+        if (db) peer_put<2>(P, L.dst, f, x, y, 0, db);
+        if (dt) peer_put<3>(P, L.dst, f, x, y, 0, dt);
+        if (dl && db) peer_put<4>(P, L.dst, f, x, y, dl, db);
+        if (dr && db) peer_put<5>(P, L.dst, f, x, y, dr, db);
+        if (dl && dt) peer_put<6>(P, L.dst, f, x, y, dl, dt);
+        if (dr && dt) peer_put<7>(P, L.dst, f, x, y, dr, dt);
     }
     if (timed_out && threadIdx.x == 0) report(L.status, TLB_ST_PEER_TIMEOUT, x, y, L.step);
     if (L.flags & TLB_F_COUNT_NEG) count_neg(L.status, f, active);
-    // The last border block to finish publishes "step done" to both
-    // neighbours: only border blocks read our halos and write theirs, so the
-    // bulk need not finish first.  Fence / counter / fence is the
-    // threadFenceReduction pattern at system scope: every border block's
-    // halo reads and remote stores precede its counter increment, and the
-    // last block's release stores follow all of them.
+    // The last border block to finish publishes "step done" to every
+    // neighbour.  Fence / counter / fence is the threadFenceReduction
+    // pattern at system scope: every border block's halo reads and remote
+    // stores precede its counter increment, and the last block's release
+    // stores follow all of them.
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence_system();
-        unsigned long long *ctr = P.mb + 2;
+        unsigned long long *ctr = P.mb + TLB_MB_COUNTER;
         if (atomicAdd(ctr, 1ull) == (unsigned long long)(P.nbb - 1)) {
             *ctr = 0;                      // next step (next kernel) starts from 0
             __threadfence_system();
             const unsigned long long v = (unsigned long long)P.need + 1;
-            // we are our left neighbour's RIGHT neighbour and vice versa
-            asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(P.left_mb + 1), "l"(v)
-                         : "memory");
-            asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(P.right_mb), "l"(v)
-                         : "memory");
+            for (int d = 0; d < 8; ++d) {
+                if (!(P.present >> d & 1)) continue;
+                // we are that neighbour's neighbour in the reverse direction
+                asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(P.nbmb[d] + POPP(d)),
+                             "l"(v) : "memory");
+            }
         }
     }
 }
@@ -197,18 +236,21 @@ int tlb_ipc_handle(const void *ptr, char *out64, int64_t *offset) {
     return TLB_OK;
 }
 
-int tlb_peer_create(int device, const char *handles, const int64_t *offsets, tlb_peer_t *out) {
+int tlb_peer_create2(int device, const char *handles, const int64_t *offsets,
+                     const int *present, tlb_peer_t *out) {
     TLB_CUDA_CHECK(cudaSetDevice(device));
     TlbPeer *p = new TlbPeer();
     p->device = device;
-    void *ptrs[6];
-    for (int k = 0; k < 6; ++k) {
+    void *ptrs[24] = {};
+    for (int k = 0; k < 24; ++k) {
+        if (!present[k / 3]) continue;
         cudaIpcMemHandle_t hd;
         memcpy(&hd, handles + 64 * k, sizeof hd);
-        // a neighbour may appear twice (Np = 2): open each distinct handle once
+        // a neighbour can sit in several directions: open each handle once
         int same = -1;
         for (int j = 0; j < k; ++j)
-            if (!memcmp(handles + 64 * j, handles + 64 * k, sizeof hd)) same = j;
+            if (present[j / 3] && !memcmp(handles + 64 * j, handles + 64 * k, sizeof hd))
+                same = j;
         if (same >= 0) {
             ptrs[k] = (char *)ptrs[same] - offsets[same];
         } else {
@@ -223,21 +265,32 @@ int tlb_peer_create(int device, const char *handles, const int64_t *offsets, tlb
         }
         ptrs[k] = (char *)ptrs[k] + offsets[k];
     }
-    p->left[0] = (double *)ptrs[0];
-    p->left[1] = (double *)ptrs[1];
-    p->left_mb = (unsigned long long *)ptrs[2];
-    p->right[0] = (double *)ptrs[3];
-    p->right[1] = (double *)ptrs[4];
-    p->right_mb = (unsigned long long *)ptrs[5];
+    for (int d = 0; d < 8; ++d) {
+        p->present[d] = present[d] != 0;
+        p->buf[d][0] = (double *)ptrs[3 * d];
+        p->buf[d][1] = (double *)ptrs[3 * d + 1];
+        p->mb[d] = (unsigned long long *)ptrs[3 * d + 2];
+    }
     *out = p;
     return TLB_OK;
+}
+
+// 1-D ring: handles/offsets = left A, left B, left mailbox, right A, right B,
+// right mailbox
+int tlb_peer_create(int device, const char *handles, const int64_t *offsets, tlb_peer_t *out) {
+    char h[24 * 64] = {};
+    int64_t o[24] = {};
+    const int present[8] = {1, 1, 0, 0, 0, 0, 0, 0};
+    memcpy(h, handles, 6 * 64);
+    memcpy(o, offsets, 6 * sizeof(int64_t));
+    return tlb_peer_create2(device, h, o, present, out);
 }
 
 int tlb_peer_destroy(tlb_peer_t p) {
     if (!p) return TLB_OK;
     cudaSetDevice(p->device);
     cudaDeviceSynchronize();
-    for (int k = 0; k < 6; ++k)
+    for (int k = 0; k < 24; ++k)
         if (p->opened[k]) cudaIpcCloseMemHandle(p->opened[k]);
     delete p;
     return TLB_OK;
@@ -251,9 +304,18 @@ int tlb_peer_step(tlb_peer_t pr, const TlbField *prv, const TlbField *nxt, int p
     if ((e = check_params(p))) return e;
     if (p->order != 4) return fail(TLB_ERR_UNSUPPORTED, "peer step: order 4 only");
     if (device_generic()) return fail(TLB_ERR_UNSUPPORTED, "peer step: D2Q37 kernels only");
-    if (flags & (TLB_F_WRAP_X)) return fail(TLB_ERR_CONTRACT, "peer step: X halos are remote");
     const int h = TLB_WALL_ROWS;
-    if (prv->Lx < 2 * h + 1) return fail(TLB_ERR_UNSUPPORTED, "peer step: tile narrower than 7");
+    const bool xb = pr->present[0] || pr->present[1];
+    const bool yb_lo = pr->present[2], yb_hi = pr->present[3];
+    if (!xb && !yb_lo && !yb_hi) return fail(TLB_ERR_CONTRACT, "peer step: no neighbours");
+    if (xb && (flags & TLB_F_WRAP_X))
+        return fail(TLB_ERR_CONTRACT, "peer step: X halos are remote");
+    if ((yb_lo || yb_hi) && (flags & TLB_F_WRAP_Y))
+        return fail(TLB_ERR_CONTRACT, "peer step: Y halos are remote");
+    if (xb && prv->Lx < 2 * h + 1)
+        return fail(TLB_ERR_UNSUPPORTED, "peer step: tile narrower than 7");
+    if ((yb_lo || yb_hi) && prv->Ly < 2 * h + 1)
+        return fail(TLB_ERR_UNSUPPORTED, "peer step: tile lower than 7");
     cudaStream_t s = (cudaStream_t)stream;
     SiteLaunch L;
     memset(&L, 0, sizeof L);
@@ -264,7 +326,10 @@ int tlb_peer_step(tlb_peer_t pr, const TlbField *prv, const TlbField *nxt, int p
     L.flags = flags;
     L.step = -1;
     wall_rows(L, prv, flags);
-    TlbRegion bulk = {prv->Hx + h, prv->Hx + prv->Lx - h, prv->Hy, prv->Hy + prv->Ly};
+    const int x0 = prv->Hx, x1 = prv->Hx + prv->Lx, y0 = prv->Hy, y1 = prv->Hy + prv->Ly;
+    const int bx0 = x0 + (xb ? h : 0), bx1 = x1 - (xb ? h : 0);
+    const int by0 = y0 + (yb_lo ? h : 0), by1 = y1 - (yb_hi ? h : 0);
+    TlbRegion bulk = {bx0, bx1, by0, by1};
     split_region(L, bulk, prv, flags);
     for (int l = 0; l < Q; ++l) {
         L.soffb[l] = 8 * ((long long)l * L.src.sl - ((long long)CX(l) * L.src.sx +
@@ -274,21 +339,34 @@ int tlb_peer_step(tlb_peer_t pr, const TlbField *prv, const TlbField *nxt, int p
     L.nfb = (L.fr_end[3] + 127) / 128;
     PeerLaunch P;
     memset(&P, 0, sizeof P);
-    P.rleft = pr->left[parity];
-    P.rright = pr->right[parity];
+    for (int d = 0; d < 8; ++d) {
+        if (!pr->present[d]) continue;
+        P.present |= 1 << d;
+        P.nb[d] = pr->buf[d][parity];
+        P.nbmb[d] = pr->mb[d];
+    }
     P.mb = mailbox;
-    P.left_mb = pr->left_mb;
-    P.right_mb = pr->right_mb;
     P.need = peer_step;
-    P.h = h;
+    P.xb = xb;
+    P.yb_lo = yb_lo;
+    P.yb_hi = yb_hi;
+    P.Hx = prv->Hx;
+    P.Hy = prv->Hy;
     P.Lx = prv->Lx;
-    P.x_left0 = prv->Hx;
-    P.x_right0 = prv->Hx + prv->Lx - h;
-    P.br[0] = mkrect(prv->Hx, prv->Hx + h, prv->Hy, prv->Hy + prv->Ly);
-    P.br[1] = mkrect(prv->Hx + prv->Lx - h, prv->Hx + prv->Lx, prv->Hy, prv->Hy + prv->Ly);
-    P.br_end[0] = P.br[0].n;
-    P.br_end[1] = P.br[0].n + P.br[1].n;
-    P.nbb = (P.br_end[1] + 127) / 128;
+    P.Ly = prv->Ly;
+    // border bands: left / right columns over the full height, then bottom /
+    // top rows between them
+    const Rect none = mkrect(0, 0, 0, 0);
+    P.br[0] = xb ? mkrect(x0, x0 + h, y0, y1) : none;
+    P.br[1] = xb ? mkrect(x1 - h, x1, y0, y1) : none;
+    P.br[2] = yb_lo ? mkrect(bx0, bx1, y0, y0 + h) : none;
+    P.br[3] = yb_hi ? mkrect(bx0, bx1, y1 - h, y1) : none;
+    unsigned acc = 0;
+    for (int k = 0; k < 4; ++k) {
+        acc += P.br[k].n;
+        P.br_end[k] = acc;
+    }
+    P.nbb = (acc + 127) / 128;
     const unsigned nb = L.nfb + (L.in.n + 127) / 128 + P.nbb;
     if (p->arith == TLB_ARITH_EXACT)
         k_peer_step<true><<<nb, 128, 0, s>>>(L, P);

@@ -411,17 +411,19 @@ class RankWorker:
             self._capture_slot = None
             self._peer = None
             # NVLink peer stores fused into the step kernel (tlb_peer_step):
-            # 1-D ring, overlapped schedule, the specialised D2Q37 order-4
-            # kernels, tiles at least 7 columns wide.  "auto" takes it when
-            # it applies, else the NCCL ring; "p2p" insists.
+            # 1-D ring or 2-D grid, overlapped schedule, the specialised
+            # D2Q37 order-4 kernels, tiles at least 7 sites across every
+            # exchanged direction.  "auto" takes it when it applies, else
+            # the NCCL ring; "p2p" insists.
             order = params.eq_order if params.eq_order is not None else vs.eq_order
-            peer_ok = (self._ring is not None and not self.y_exchange and not self.x_self
+            peer_ok = (self._ring is not None and (not self.x_self or self.y_exchange)
                        and schedule == "overlapped" and vs.Q == 37 and order == 4
-                       and tile.Lx >= 7)
+                       and (self.x_self or tile.Lx >= 7)
+                       and (not self.y_exchange or tile.Ly >= 7))
             if exchange == "p2p" and not peer_ok and self._ring is not None:
                 raise ConfigurationError(
-                    "exchange='p2p' needs a 1-D ring of D2Q37 order-4 tiles >= 7 columns "
-                    "wide with the overlapped schedule")
+                    "exchange='p2p' needs D2Q37 order-4 tiles >= 7 sites across each "
+                    "exchanged direction with the overlapped schedule")
             if exchange in ("auto", "p2p") and peer_ok:
                 self._setup_peer(fabric, strict=exchange == "p2p")
             # order the allocations' zero-fills before any work on our stream
@@ -448,10 +450,10 @@ class RankWorker:
         import warnings
         torch = _lib.torch_cuda()
         lib = _lib.load()
-        # [0] left neighbour's step, [1] right neighbour's step (written by
-        # them), [2] this rank's border-block counter, [3] sticky timeout
-        # flag (tlb_peer_step)
-        self.mailbox = torch.zeros(4, dtype=torch.int64, device=self.device)
+        # [0..7] step published by the neighbour in direction d (written by
+        # them), [8] this rank's border-block counter, [9] sticky timeout
+        # flag (csrc/tlb_peer.cuh)
+        self.mailbox = torch.zeros(16, dtype=torch.int64, device=self.device)
         torch.cuda.synchronize(self.device)
 
         def agree(ok, why):
@@ -479,14 +481,16 @@ class RankWorker:
         fabric.dist.all_gather_object(allinfo, mine, group=fabric.group)
         if not agree(mine is not None, why):
             return
-        nb = self.tile.neighbors
-        order = allinfo[nb["left"]] + allinfo[nb["right"]]
+        ranks = self._peer_neighbours()
+        blank = (b"\0" * 64, 0)
+        order = [item for r in ranks for item in (allinfo[r] if r is not None else [blank] * 3)]
         handles = b"".join(h for h, _ in order)
-        offs = (ctypes.c_int64 * 6)(*[o for _, o in order])
+        offs = (ctypes.c_int64 * 24)(*[o for _, o in order])
+        present = (ctypes.c_int * 8)(*[int(r is not None) for r in ranks])
         hp = ctypes.c_void_p()
         try:
-            _lib.check(lib.tlb_peer_create(self.device.index, handles, offs, ctypes.byref(hp)),
-                       "peer create")
+            _lib.check(lib.tlb_peer_create2(self.device.index, handles, offs, present,
+                                            ctypes.byref(hp)), "peer create")
             ok, why = True, ""
         except ThermoLBError as exc:
             ok, why = False, str(exc)
@@ -499,6 +503,23 @@ class RankWorker:
         self._peer_step = 0
         self._primed = False
         fabric.dist.barrier(group=fabric.group)
+
+    # the eight directions of csrc/tlb_peer.cuh: (dx, dy)
+    _PEER_DIRS = ((-1, 0), (1, 0), (0, -1), (0, 1), (-1, -1), (1, -1), (-1, 1), (1, 1))
+
+    def _peer_neighbours(self):
+        """Rank of the neighbour in each peer direction, None where that side
+        is not exchanged (self-periodic X or Y, or a wall)."""
+        nx, ny = self.tile.grid
+        ix, iy = self.tile.coords
+        out = []
+        for dx, dy in self._PEER_DIRS:
+            if (dx and self.x_self) or (dy < 0 and not self.ex_down) or \
+                    (dy > 0 and not self.ex_up):
+                out.append(None)
+                continue
+            out.append(((iy + dy) % ny) * nx + (ix + dx) % nx)
+        return out
 
     # -- helpers -------------------------------------------------------------
     @property

@@ -42,6 +42,9 @@ def main():
     cases = [(t, sch, "nccl") for t in tilings for sch in ("overlapped", "staged")]
     cases.append(("1d", "overlapped", "p2p"))      # NVLink peer-store exchange
     cases.append(("1d", "overlapped", "auto"))     # the default (p2p where it applies)
+    cases.append(((1, world), "overlapped", "p2p"))  # Y split only: X self-periodic
+    if world >= 4:
+        cases.append(((2, world // 2), "overlapped", "p2p"))   # 2-D: corners diagonal
     ok = True
     for tiling, schedule, exchange in cases:
         for arith in (("exact", "fast") if exchange == "p2p" else ("exact",)):
