@@ -338,12 +338,9 @@ __device__ __forceinline__ double div_rcp2(double x, double b, double y) {
 // divisions share one correctly rounded reciprocal of rho (and of 2 rho,
 // which is exactly half of it) and are completed by Markstein corrections:
 // bit for bit the IEEE quotients of the reference.
-template <class F>
-__device__ __forceinline__ bool moments_exact(const F &f, double &rho, double &ux,
-                                              double &uy, double &T) {
-    double r = 0.0, mx = 0.0, my = 0.0, e2 = 0.0;
-    MomSeq<0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16, 17, 18, 19, 20,
-           21, 22, 23, 24, 25, 26, 27, 28, 29, 30, 31, 32, 33, 34, 35, 36>::run(f, r, mx, my, e2);
+// The divisions of moments (kernels.py:55-71) given the fixed-order sums.
+__device__ __forceinline__ bool moments_tail(double r, double mx, double my, double e2,
+                                             double &rho, double &ux, double &uy, double &T) {
     rho = r;
     if (!(r > 1e-300 && r < 1e300)) {  // degenerate or extreme: plain IEEE division
         ux = __ddiv_rn(mx, r);
@@ -357,6 +354,15 @@ __device__ __forceinline__ bool moments_exact(const F &f, double &rho, double &u
     T = div_rcp2(dsub(e2, dmul(r, dadd(dmul(ux, ux), dmul(uy, uy)))), dmul(2.0, r),
                  dmul(0.5, yr));
     return true;
+}
+
+template <class F>
+__device__ __forceinline__ bool moments_exact(const F &f, double &rho, double &ux,
+                                              double &uy, double &T) {
+    double r = 0.0, mx = 0.0, my = 0.0, e2 = 0.0;
+    MomSeq<0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16, 17, 18, 19, 20,
+           21, 22, 23, 24, 25, 26, 27, 28, 29, 30, 31, 32, 33, 34, 35, 36>::run(f, r, mx, my, e2);
+    return moments_tail(r, mx, my, e2, rho, ux, uy, T);
 }
 
 // collide one site in place (kernels.py:139-146).  Returns TLB_ST_* bits.
