@@ -14,6 +14,7 @@ struct GenConst {
     int cx[GQ], cy[GQ];
     double w[GQ], ex[GQ], ey[GQ], q[GQ];
     double cs, cs2;
+    double rcs, rcs2, r6, r24;  // RN reciprocals for the Markstein divisions
 };
 
 __constant__ GenConst G;
@@ -51,11 +52,9 @@ __device__ __forceinline__ void gen_moments(const double (&f)[NQ], double &rho, 
         const double c2 = __dadd_rn(__dmul_rn(cx, cx), __dmul_rn(cy, cy));
         if (c2 != 0.0) e2 = __dadd_rn(e2, __dmul_rn(c2, f[l]));
     }
-    rho = r;
-    ux = __ddiv_rn(mx, r);
-    uy = __ddiv_rn(my, r);
-    T = __ddiv_rn(__dsub_rn(e2, __dmul_rn(r, __dadd_rn(__dmul_rn(ux, ux), __dmul_rn(uy, uy)))),
-                  __dmul_rn(2.0, r));
+    // the three divisions, correctly rounded via one reciprocal and
+    // Markstein corrections (d2q37.cuh: same bits as __ddiv_rn)
+    moments_tail(r, mx, my, e2, rho, ux, uy, T);
 }
 
 // equilibrium, kernels.py:87-124, written term by term in the reference's
@@ -64,8 +63,9 @@ template <int NQ>
 __device__ __forceinline__ void gen_equilibrium(double rho, double ux, double uy, double T,
                                                 int order, double (&out)[NQ]) {
     const double D = 2.0;
-    const double vx = __ddiv_rn(ux, G.cs), vy = __ddiv_rn(uy, G.cs);
-    const double th = __dsub_rn(__ddiv_rn(T, G.cs2), 1.0);
+    // correctly rounded divisions by the constants cs, cs2, 6, 24
+    const double vx = div_const2(ux, G.cs, G.rcs), vy = div_const2(uy, G.cs, G.rcs);
+    const double th = __dsub_rn(div_const2(T, G.cs2, G.rcs2), 1.0);
     const double s = __dadd_rn(__dmul_rn(vx, vx), __dmul_rn(vy, vy));
 #pragma unroll
     for (int l = 0; l < NQ; ++l) {
@@ -79,7 +79,7 @@ __device__ __forceinline__ void gen_equilibrium(double rho, double ux, double uy
             const double c3 = __dsub_rn(
                 __dadd_rn(__dmul_rn(pp, p), __dmul_rn(__dmul_rn(__dmul_rn(3.0, th), q), p)),
                 __dmul_rn(__dmul_rn(3.0, p), __dadd_rn(s, __dmul_rn(D + 2.0, th))));
-            poly = __dadd_rn(poly, __ddiv_rn(c3, 6.0));
+            poly = __dadd_rn(poly, div_const1(c3, 6.0, G.r6));
         }
         if (order >= 4) {
             const double A = __dmul_rn(__dmul_rn(pp, p), p);
@@ -95,7 +95,7 @@ __device__ __forceinline__ void gen_equilibrium(double rho, double ux, double uy
                 __dmul_rn(__dmul_rn(D * (D + 2.0), th), th));
             const double c4 = __dadd_rn(__dsub_rn(__dadd_rn(__dadd_rn(A, B), Cc), __dmul_rn(6.0, in6)),
                                         __dmul_rn(3.0, in3));
-            poly = __dadd_rn(poly, __ddiv_rn(c4, 24.0));
+            poly = __dadd_rn(poly, div_const1(c4, 24.0, G.r24));
         }
         out[l] = __dmul_rn(__dmul_rn(G.w[l], rho), poly);
     }

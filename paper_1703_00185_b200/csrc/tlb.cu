@@ -724,6 +724,10 @@ static int set_generic(int device, int nq, const int64_t *c, const double *w, do
     g.Q = nq;
     g.cs2 = cs2;
     g.cs = std::sqrt(cs2);
+    g.rcs = 1.0 / g.cs;
+    g.rcs2 = 1.0 / cs2;
+    g.r6 = 1.0 / 6.0;
+    g.r24 = 1.0 / 24.0;
     GenHost &hst = g_gen[device];
     hst.Q = nq;
     for (int l = 0; l < nq; ++l) {
