@@ -135,20 +135,30 @@ __device__ __forceinline__ void gen_count_neg(TlbStatus *st, const double (&f)[N
     count_neg_n(st, n);
 }
 
-template <int KIND, int NQ, bool INPLACE>
+template <int KIND, int NQ, bool INPLACE, bool EDGE>
 __device__ __forceinline__ void gen_body(const SiteLaunch &L, int x, int y, bool active) {
     double f[NQ];
     const bool gather = KIND == K_PROPAGATE || KIND == K_FUSED;
     const Fld &s = L.src;
+    if (!EDGE && !INPLACE) {
+        // interior: the launch's precomputed (shifted) byte offsets, no remapping
+        const char *sp = reinterpret_cast<const char *>(s.base + (long long)x * s.sx +
+                                                        (long long)y * s.sy);
 #pragma unroll
-    for (int l = 0; l < NQ; ++l) {
-        int xs = x, ys = y;
-        if (gather && !INPLACE) {
-            xs = src_x(x, G.cx[l], s, L.flags);
-            ys = src_y(y, G.cy[l], s, L.flags);
+        for (int l = 0; l < NQ; ++l)
+            f[l] = __ldg(reinterpret_cast<const double *>(sp + L.soffb[l]));
+    } else {
+#pragma unroll
+        for (int l = 0; l < NQ; ++l) {
+            int xs = x, ys = y;
+            if (gather && !INPLACE) {
+                xs = src_x(x, G.cx[l], s, L.flags);
+                ys = src_y(y, G.cy[l], s, L.flags);
+            }
+            const double *p = s.base + (long long)l * s.sl + (long long)xs * s.sx +
+                              (long long)ys * s.sy;
+            f[l] = INPLACE ? *p : __ldg(p);
         }
-        const double *p = s.base + (long long)l * s.sl + (long long)xs * s.sx + (long long)ys * s.sy;
-        f[l] = INPLACE ? *p : __ldg(p);
     }
     unsigned bits = 0;
     if (KIND == K_BC || KIND == K_FUSED) {
@@ -178,18 +188,27 @@ __global__ void __launch_bounds__(128) k_gen_site(const __grid_constant__ SiteLa
         const int r = ii < L.fr_end[0] ? 0 : ii < L.fr_end[1] ? 1 : ii < L.fr_end[2] ? 2 : 3;
         const unsigned loc = ii - (r ? L.fr_end[r - 1] : 0u);
         const Rect &R = L.fr[r];
-        gen_body<KIND, NQ, INPLACE>(L, R.x0 + (int)(loc / R.ny), R.y0 + (int)(loc % R.ny), active);
+        gen_body<KIND, NQ, INPLACE, true>(L, R.x0 + (int)(loc / R.ny), R.y0 + (int)(loc % R.ny),
+                                          active);
     } else {
         const unsigned i = (blockIdx.x - L.nfb) * blockDim.x + threadIdx.x;
         const bool active = i < L.in.n;
         const unsigned ii = active ? i : L.in.n - 1;
-        gen_body<KIND, NQ, INPLACE>(L, L.in.x0 + (int)(ii / L.in.ny), L.in.y0 + (int)(ii % L.in.ny),
-                                    active);
+        gen_body<KIND, NQ, INPLACE, false>(L, L.in.x0 + (int)(ii / L.in.ny),
+                                           L.in.y0 + (int)(ii % L.in.ny), active);
     }
 }
 
 template <int KIND, bool INPLACE>
 static int launch_gen(SiteLaunch &L, int Q, cudaStream_t s, const char *what) {
+    const GenHost &gh = gen_host();
+    constexpr bool gather = KIND == K_PROPAGATE || KIND == K_FUSED;
+    for (int l = 0; l < Q; ++l) {   // interior gather offsets, as launch_site does for D2Q37
+        long long so = (long long)l * L.src.sl;
+        if (gather) so -= (long long)gh.cx[l] * L.src.sx + (long long)gh.cy[l] * L.src.sy;
+        L.soffb[l] = 8 * so;
+        L.doffb[l] = 8 * (long long)l * L.dst.sl;
+    }
     const unsigned long long nf = L.fr_end[3];
     L.nfb = (unsigned)((nf + 127) / 128);
     const unsigned long long nb = L.nfb + (L.in.n + 127ULL) / 128;
