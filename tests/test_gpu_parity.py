@@ -330,3 +330,36 @@ def test_rt256_1000_steps_exact_bitwise_and_fast_drift(vs, runs, rt256, orc):
     rel = np.max(np.abs(fast - want) / np.abs(want))
     print("fast drift after 1000 steps:", rel)
     assert rel < 1e-12
+
+
+@pytest.mark.parametrize("case", range(24))
+def test_randomised_configs_bitwise(vs, orc, case):
+    """Seeded random configurations through run() against the C oracle,
+    bitwise: lattice shape, tau, body force, wall temperatures, walls or
+    periodic Y, rank count and tiling (in-process ranks), schedule,
+    storage layout, random or Rayleigh-Taylor start, 1-9 steps."""
+    rng = np.random.default_rng(1000 + case)
+    periodic = bool(rng.integers(2))
+    tiling_choice = int(rng.integers(3))
+    Np, tiling = [(1, "1d"), (2, "1d"), (4, (2, 2))][tiling_choice]
+    nx, ny = (Np, 1) if tiling == "1d" else tiling
+    Lx = nx * int(rng.integers(7, 40))
+    Ly = ny * int(rng.integers(7, 40))
+    tau = float(rng.uniform(0.55, 2.0))
+    gx, gy = (float(v) for v in rng.normal(0.0, 2e-5, 2))
+    Tt, Tb = (float(v) * vs.cs2 for v in rng.uniform(0.85, 1.15, 2))
+    p = tl.PhysicsParams(tau=tau, gx=gx, gy=gy, Twall_top=Tt, Twall_bot=Tb)
+    init = ["random", "rayleigh-taylor"][int(rng.integers(2))]
+    steps = int(rng.integers(1, 10))
+    res = tl.run(tl.SimConfig(
+        Lx=Lx, Ly=Ly, Np=Np, tiling=tiling, steps=steps, params=p, init=init,
+        init_kwargs={"seed": case} if init == "random" else {},
+        walls=not periodic, periodic_y=periodic,
+        schedule=["overlapped", "staged"][int(rng.integers(2))],
+        layout=["column", "soa", "aos"][int(rng.integers(3))]))
+    f0 = tl.init.build_initial_state(init, Lx, Ly, vs,
+                                     **({"seed": case} if init == "random" else {}))
+    want, _ = orc.run(f0.cpu().numpy(), steps,
+                      orc.params6(tau, gx, gy, 1.0, Tt, Tb),
+                      ymode="periodic" if periodic else "walls")
+    assert np.array_equal(res.populations, want), (case, Lx, Ly, Np, tiling, periodic)
