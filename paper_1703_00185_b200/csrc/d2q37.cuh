@@ -88,25 +88,12 @@ __constant__ StencilConst C;
 
 // Population accessors: the arithmetic below reads f_l through get(l) and
 // writes results through put(l, v), so the same code runs on a
-// register-resident 37-vector (RegF) or on a shared-memory tile with the
-// results streamed straight to global memory (SmemF).
+// register-resident 37-vector (RegF) or streams each output straight to
+// global memory as soon as it is final (RegStoreF in tlb.cu).
 struct RegF {
     double (&a)[Q];
     __device__ __forceinline__ double get(int l) const { return a[l]; }
     __device__ __forceinline__ void put(int l, double v) { a[l] = v; }
-};
-
-struct SmemF {
-    const double *s;  // this site's column in the staged tile, stride `ss`
-    int ss;
-    double *o;        // this site's output address, population stride `os`
-    long long os;
-    unsigned neg;     // negative outputs written (count_negative)
-    __device__ __forceinline__ double get(int l) const { return s[l * ss]; }
-    __device__ __forceinline__ void put(int l, double v) {
-        o[(long long)l * os] = v;
-        neg += v < 0.0;
-    }
 };
 
 // ---------------------------------------------------------------- exact --
