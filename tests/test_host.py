@@ -224,3 +224,37 @@ def test_planner_limits():
         P.CostModelInput(0, 10, 1, 1e9, 1e9, 1e-8)
     rows = P.scaling_curve(P.CostModelInput(512, 512, 1, 1e11, 1e11, 1e-10), [1, 2, 4])
     assert {r[1] for r in rows} == {"1d", "2d", "1d_overlap", "2d_overlap"}
+
+
+def test_peer_neighbour_directions():
+    """RankWorker._peer_neighbours: rank in each of the 8 peer directions
+    (left, right, down, up, down-left, down-right, up-left, up-right),
+    None where the side is self-periodic or a wall (csrc/tlb_peer.cuh)."""
+    from types import SimpleNamespace
+    from paper_1703_00185_b200.runtime import RankWorker
+
+    def dirs(Lx, Ly, Np, tiling, periodic_y=False):
+        out = []
+        for t in tl.decompose(Lx, Ly, Np, tiling, periodic_y=periodic_y):
+            nb = t.neighbors
+            y_self = t.grid[1] == 1 and nb["up"] is not None
+            w = SimpleNamespace(tile=t, x_self=nb["left"] == t.rank,
+                                ex_up=nb["up"] is not None and not y_self,
+                                ex_down=nb["down"] is not None and not y_self,
+                                _PEER_DIRS=RankWorker._PEER_DIRS)
+            out.append(RankWorker._peer_neighbours(w))
+        return out
+
+    # 1-D ring of 4 with walls: left/right only
+    assert dirs(64, 16, 4, "1d")[1] == [0, 2, None, None, None, None, None, None]
+    # 2x2 grid with walls: rank 0 (bottom-left) has right/up/up-right (= 1, 2, 3)
+    # and, X being periodic, the same ranks on the left side
+    d = dirs(32, 32, 4, (2, 2))
+    assert d[0] == [1, 1, None, 2, None, None, 3, 3]
+    assert d[3] == [2, 2, 1, None, 0, 0, None, None]
+    # (1, 4) grid, periodic Y: X self-periodic -> only down/up
+    d = dirs(16, 64, 4, (1, 4), periodic_y=True)
+    assert d[0] == [None, None, 3, 1, None, None, None, None]
+    # 3x3 periodic: all 8 distinct neighbours of the centre rank
+    d = dirs(36, 36, 9, (3, 3), periodic_y=True)
+    assert d[4] == [3, 5, 1, 7, 0, 2, 6, 8]
