@@ -36,8 +36,9 @@ def main():
         from oracle import oracle as O
         O.set_stencil(vs.c, vs.w, vs.cs2)
         f0 = O.equilibrium(*O.rayleigh_taylor_macro(Lx, Ly, vs.cs2))
-        want, neg = O.run(f0, steps, O.params6(p.tau, p.gx, p.gy, p.dt, p.Twall_top,
-                                                 p.Twall_bot))
+        p6 = O.params6(p.tau, p.gx, p.gy, p.dt, p.Twall_top, p.Twall_bot)
+        want, neg = O.run(f0, steps, p6)
+        want_periodic, _ = O.run(f0, steps, p6, ymode="periodic")
     tilings = ["1d", (1, world)] + ([(2, world // 2)] if world >= 4 else [])
     cases = [(t, sch, "nccl") for t in tilings for sch in ("overlapped", "staged")]
     cases.append(("1d", "overlapped", "p2p"))      # NVLink peer-store exchange
@@ -45,21 +46,30 @@ def main():
     cases.append(((1, world), "overlapped", "p2p"))  # Y split only: X self-periodic
     if world >= 4:
         cases.append(((2, world // 2), "overlapped", "p2p"))   # 2-D: corners diagonal
+    cases = [c + (False,) for c in cases]
+    # periodic Y: up/down neighbours wrap (2-D: the same rank above and below)
+    cases.append(((1, world), "overlapped", "p2p", True))
+    if world >= 4:
+        cases.append(((2, world // 2), "overlapped", "p2p", True))
+        cases.append(((2, world // 2), "overlapped", "nccl", True))
     ok = True
-    for tiling, schedule, exchange in cases:
+    for tiling, schedule, exchange, periodic in cases:
         for arith in (("exact", "fast") if exchange == "p2p" else ("exact",)):
             pp = tl.PhysicsParams(tau=p.tau, gx=p.gx, gy=p.gy, Twall_top=p.Twall_top,
                                   Twall_bot=p.Twall_bot, arith=arith)
             res = tl.run(tl.SimConfig(Lx=Lx, Ly=Ly, Np=world, tiling=tiling, steps=steps,
                                       params=pp, init="rayleigh-taylor", schedule=schedule,
-                                      exchange=exchange))
+                                      exchange=exchange, walls=not periodic,
+                                      periodic_y=periodic))
             if rank == 0:
+                ref = want_periodic if periodic else want
                 if arith == "exact":
-                    same = np.array_equal(res.populations, want)
+                    same = np.array_equal(res.populations, ref)
                 else:
-                    same = bool(np.max(np.abs(res.populations - want) / np.abs(want)) < 1e-12)
+                    same = bool(np.max(np.abs(res.populations - ref) / np.abs(ref)) < 1e-12)
                 print(f"tiling={tiling} schedule={schedule} exchange={exchange} arith={arith} "
-                      f"world={world} ok={same} mlups={res.mlups:.1f}", flush=True)
+                      f"periodic={periodic} world={world} ok={same} mlups={res.mlups:.1f}",
+                      flush=True)
                 ok &= same
             assert len(res.metrics) == steps
     dist.barrier()
