@@ -152,8 +152,17 @@ __global__ void __launch_bounds__(128, 4)
     const Rect &R = P.br[r];
     const int x = R.x0 + (int)(loc / R.ny), y = R.y0 + (int)(loc % R.ny);
     double f[Q];
-    const bool implicit = (L.flags & (TLB_F_WRAP_X | TLB_F_WRAP_Y | TLB_F_CLAMP_Y)) != 0;
-    load_all(f, L.src, x, y, true, implicit, L.flags);
+    // the halos are in memory (neighbours' stores); only sites within 3 of a
+    // self-periodic or wall edge need the implicit remapping -- the rest of
+    // the (tall) bands take the branch-free gather of the interior
+    const int h = TLB_WALL_ROWS;
+    const bool remap_x = (L.flags & TLB_F_WRAP_X) && (x < P.Hx + h || x >= P.Hx + P.Lx - h);
+    const bool remap_y = (L.flags & (TLB_F_WRAP_Y | TLB_F_CLAMP_Y)) &&
+                         (y < P.Hy + h || y >= P.Hy + P.Ly - h);
+    if (remap_x || remap_y)
+        load_all(f, L.src, x, y, true, true, L.flags);
+    else
+        load_plain<false>(f, L, x, y);
     unsigned bits = 0;
     {
         const bool bot = y >= L.bot_lo && y < L.bot_hi;
@@ -174,7 +183,6 @@ __global__ void __launch_bounds__(128, 4)
         // depth of this site inside each exchanged band (0 = not in it).  No
         // per-thread fence: the block barrier + one fence.sys before the
         // border counter below order these stores before the release.
-        const int h = TLB_WALL_ROWS;
         const int dl = P.xb && x < P.Hx + h ? x - P.Hx + 1 : 0;
         const int dr = P.xb && x >= P.Hx + P.Lx - h ? P.Hx + P.Lx - x : 0;
         const int db = P.yb_lo && y < P.Hy + h ? y - P.Hy + 1 : 0;

@@ -424,16 +424,6 @@ class RankWorker:
                 raise ConfigurationError(
                     "exchange='p2p' needs D2Q37 order-4 tiles >= 7 sites across each "
                     "exchanged direction with the overlapped schedule")
-            # "auto" keeps the ring for tall tiles: the peer step runs its
-            # border blocks first, and once they exceed one wave of CTAs
-            # (e.g. 2048x16384 tiles of the strong-scaling C4 lattice) the
-            # ring's fully overlapped side-stream exchange is ~1 % faster
-            # (profiles/r01_summary.md); below that the peer step wins ~2 %.
-            border = ((0 if self.x_self else 6 * tile.Ly)
-                      + (3 * tile.Lx if self.ex_up else 0) + (3 * tile.Lx if self.ex_down else 0))
-            one_wave = 4 * 128 * torch.cuda.get_device_properties(self.device).multi_processor_count
-            if exchange == "auto" and border > one_wave:
-                peer_ok = False
             if exchange in ("auto", "p2p") and peer_ok:
                 self._setup_peer(fabric, strict=exchange == "p2p")
             # order the allocations' zero-fills before any work on our stream
