@@ -51,6 +51,7 @@ typedef struct CUstream_st *tlb_stream_t; /* == cudaStream_t */
 #define TLB_ST_SHIFT 2u      /* T_bar <= 0 in apply_shift     kernels.py:134-135 */
 #define TLB_ST_EQ_DOMAIN 4u  /* rho<=0 or T<=0, checked eq.   kernels.py:85-86   */
 #define TLB_ST_PEER_TIMEOUT 8u /* peer step: a neighbour did not publish in time */
+#define TLB_ST_PROTOCOL 16u    /* halo from a mis-sequenced step  runtime.py:151-154 */
 
 /* field view */
 typedef struct TlbField {
@@ -93,6 +94,7 @@ typedef struct TlbStatus {
 #define TLB_F_COUNT_NEG 32 /* add count of written f<0 to status->negatives    */
 #define TLB_F_CLAMP_TOP 64 /* read the top Y halo as the wall-row extension    */
 #define TLB_F_CLAMP_Y (TLB_F_CLAMP_BOT | TLB_F_CLAMP_TOP)
+#define TLB_F_POISON_HALOS 128 /* peer step, debug: NaN prv's halos once read (runtime.py:288-294) */
 
 /* library */
 int tlb_version(void);
@@ -231,22 +233,26 @@ int tlb_ring_abort(tlb_ring_t ring);
  * exchanges Y faces first (physical columns), then X faces (full height, so
  * corner halos carry diagonal data, runtime.py:8-12).  ybuf holds the two
  * Y payloads (tlb_face_payload_len_y each) for sending and two for
- * receiving: 4 * 26 * Lx doubles. */
+ * receiving: 4 * (26 * Lx + 1) doubles (each payload ends with its step
+ * tag). */
 int tlb_ring_set_neighbors(tlb_ring_t ring, int left, int right, int up,
                            int down, double *ybuf);
 /* pack both X faces of f (ymode as tlb_pack_x), exchange with the ring
  * neighbours, unpack into the X halo columns; sbuf/rbuf hold 2 payloads
- * (tlb_face_payload_len each, +x face first). */
+ * of tlb_face_payload_len + 1 doubles each (+x face first; the last double
+ * of each is the sender's step tag). */
 int tlb_ring_exchange(tlb_ring_t ring, const TlbField *f, int ymode,
                       double *sbuf, double *rbuf, tlb_stream_t stream);
 /* One overlapped time step: pack -> NCCL exchange (side stream) || bulk
  * fused kernel (stream) -> unpack + border columns (side stream) -> join.
  * flags as tlb_fused without TLB_F_WRAP_X.  ev_bulk0/1 (cudaEvent_t or NULL)
- * are recorded around the bulk kernel on `stream`. */
+ * are recorded around the bulk kernel on `stream`.  step_tag travels with
+ * every payload; a received tag other than ours sets TLB_ST_PROTOCOL
+ * (Fabric.recv's step check, runtime.py:151-154). */
 int tlb_ring_step(tlb_ring_t ring, const TlbField *prv, const TlbField *nxt,
                   const TlbParams *p, int flags, TlbStatus *status,
                   double *sbuf, double *rbuf, void *ev_bulk0, void *ev_bulk1,
-                  tlb_stream_t stream);
+                  int64_t step_tag, tlb_stream_t stream);
 
 /* ---- X-halo exchange fused into the step over NVLink peer memory --------
  * (1-D ring or 2-D grid, one process per GPU; runtime.py:226-284 pbc_nc /
@@ -271,14 +277,36 @@ int tlb_peer_create(int device, const char *handles, const int64_t *offsets,
 int tlb_peer_create2(int device, const char *handles, const int64_t *offsets,
                      const int *present, tlb_peer_t *out);
 int tlb_peer_destroy(tlb_peer_t peer);
+/* In-process neighbours (several ranks driven by one process, on one or
+ * several GPUs): ptrs[3*d .. 3*d+2] = neighbour d's buffer A, buffer B and
+ * mailbox (plain device pointers); peer access is enabled where needed. */
+int tlb_peer_create_local(int device, void *const *ptrs, const int *present,
+                          tlb_peer_t *out);
+/* Bound of the border blocks' wait for a neighbour (default 5 s); the host
+ * passes its fabric timeout (SimConfig.recv_timeout, sim.py:40). */
+int tlb_peer_set_timeout(tlb_peer_t peer, double seconds);
 /* One step.  nxt_index: 0 if nxt is buffer A, 1 if B.  mailbox: this rank's
- * zeroed device mailbox of >= 10 u64 ([0..7] step published by the
- * neighbour in direction d, [8] border-block counter, [9] sticky timeout).
- * peer_step: 0, 1, 2, ... (border blocks wait for mailbox >= peer_step). */
+ * zeroed device mailbox of >= 10 u64 ([0..7] value published by the
+ * neighbour in direction d, [8] border-block counter, [9] sticky failure).
+ * peer_step: 0, 1, 2, ... (border blocks wait for mailbox count >=
+ * peer_step).  step_tag: the step number, published with the step and
+ * checked against the neighbours' (TLB_ST_PROTOCOL on a mismatch, the
+ * ProtocolError of Fabric.recv, runtime.py:151-154); check_prev: our
+ * previous launch was step step_tag-1, so a neighbour still at our count
+ * must carry that tag too.  flags may add TLB_F_POISON_HALOS. */
 int tlb_peer_step(tlb_peer_t peer, const TlbField *prv, const TlbField *nxt,
                   int nxt_index, const TlbParams *p, int flags,
                   TlbStatus *status, unsigned long long *mailbox,
-                  int64_t peer_step, tlb_stream_t stream);
+                  int64_t peer_step, int64_t step_tag, int check_prev,
+                  tlb_stream_t stream);
+/* Halo fill before the first step after a (re)load: the border sites push
+ * their prv values into the neighbours' prv halos (exactly the lines the
+ * step pushes) and publish as step step_tag (= first step - 1); counts as a
+ * peer step.  prv_index: 0 if prv is buffer A, 1 if B. */
+int tlb_peer_prime(tlb_peer_t peer, const TlbField *prv, int prv_index,
+                   const TlbParams *p, TlbStatus *status,
+                   unsigned long long *mailbox, int64_t peer_step,
+                   int64_t step_tag, tlb_stream_t stream);
 
 /* Snapshot image (io.write_pgm, io.py:13-24): min-max normalised 8-bit
  * quantisation of a (nx, ny) field with row stride ld into img (nx*ny bytes,

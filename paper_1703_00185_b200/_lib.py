@@ -21,10 +21,11 @@ LIB_PATH = os.environ.get("TLB_LIB_PATH") or os.path.join(HERE, "libtlb.so")
 TLB_OK, TLB_ERR_CONTRACT, TLB_ERR_CUDA, TLB_ERR_STENCIL, TLB_ERR_UNSUPPORTED, \
     TLB_ERR_DOMAIN = range(6)
 
-ST_DEGENERATE, ST_SHIFT, ST_EQ_DOMAIN, ST_PEER_TIMEOUT = 1, 2, 4, 8
+ST_DEGENERATE, ST_SHIFT, ST_EQ_DOMAIN, ST_PEER_TIMEOUT, ST_PROTOCOL = 1, 2, 4, 8, 16
 
 F_WALL_BOT, F_CLAMP_BOT, F_WALL_TOP, F_WRAP_X, F_WRAP_Y, F_COUNT_NEG, F_CLAMP_TOP = \
     1, 4, 2, 8, 16, 32, 64
+F_POISON_HALOS = 128
 F_CLAMP_Y = F_CLAMP_BOT | F_CLAMP_TOP
 
 ARITH = {"exact": 0, "fast": 1}
@@ -100,12 +101,15 @@ SIGNATURES = [
     ("tlb_ring_abort", _INT, [_P]),
     ("tlb_ring_set_neighbors", _INT, [_P, _INT, _INT, _INT, _INT, _P]),
     ("tlb_ring_exchange", _INT, [_P, _FP, _INT, _P, _P, _P]),
-    ("tlb_ring_step", _INT, [_P, _FP, _FP, _PP, _INT, _P, _P, _P, _P, _P, _P]),
+    ("tlb_ring_step", _INT, [_P, _FP, _FP, _PP, _INT, _P, _P, _P, _P, _P, _I64, _P]),
     ("tlb_ipc_handle", _INT, [_P, ctypes.c_char_p, ctypes.POINTER(_I64)]),
     ("tlb_peer_create", _INT, [_INT, ctypes.c_char_p, _P, ctypes.POINTER(_P)]),
     ("tlb_peer_create2", _INT, [_INT, ctypes.c_char_p, _P, _P, ctypes.POINTER(_P)]),
     ("tlb_peer_destroy", _INT, [_P]),
-    ("tlb_peer_step", _INT, [_P, _FP, _FP, _INT, _PP, _INT, _P, _P, _I64, _P]),
+    ("tlb_peer_create_local", _INT, [_INT, _P, _P, ctypes.POINTER(_P)]),
+    ("tlb_peer_set_timeout", _INT, [_P, ctypes.c_double]),
+    ("tlb_peer_step", _INT, [_P, _FP, _FP, _INT, _PP, _INT, _P, _P, _I64, _I64, _INT, _P]),
+    ("tlb_peer_prime", _INT, [_P, _FP, _INT, _PP, _P, _P, _I64, _I64, _P]),
     ("tlb_pgm_image", _INT, [_P, _I64, _I64, _I64, _P, _P, _P]),
     ("tlb_set_tuning", _INT, [_INT, _INT]),
     ("tlb_bench_dfma", _INT, [_I64, ctypes.POINTER(ctypes.c_double), _P]),

@@ -165,7 +165,9 @@ __device__ __forceinline__ int src_y(int y, int cy, const Fld &s, int flags) {
     return ys;
 }
 
-template <int l>
+// COH: coherent L2 loads (ld.global.cg) for data other GPUs write while the
+// kernel runs (the peer step's halos); else the read-only path (__ldg).
+template <int l, bool COH = false>
 __device__ __forceinline__ void load_one(double (&f)[Q], const Fld &s, int x, int y,
                                          bool gather, bool implicit, int flags) {
     int xs = x, ys = y;
@@ -179,20 +181,21 @@ __device__ __forceinline__ void load_one(double (&f)[Q], const Fld &s, int x, in
         }
     }
     const double *p = s.base + (long long)l * s.sl + (long long)xs * s.sx + (long long)ys * s.sy;
-    f[l] = __ldg(p);
+    f[l] = COH ? __ldcg(p) : __ldg(p);
 }
 
-template <int... Ls>
+template <bool COH, int... Ls>
 struct LoadSeq {
     __device__ __forceinline__ static void run(double (&f)[Q], const Fld &s, int x, int y,
                                                bool gather, bool implicit, int flags) {
-        (load_one<Ls>(f, s, x, y, gather, implicit, flags), ...);
+        (load_one<Ls, COH>(f, s, x, y, gather, implicit, flags), ...);
     }
 };
 
+template <bool COH = false>
 __device__ __forceinline__ void load_all(double (&f)[Q], const Fld &s, int x, int y,
                                          bool gather, bool implicit, int flags) {
-    LoadSeq<0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16, 17, 18, 19, 20, 21,
+    LoadSeq<COH, 0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16, 17, 18, 19, 20, 21,
             22, 23, 24, 25, 26, 27, 28, 29, 30, 31, 32, 33, 34, 35,
             36>::run(f, s, x, y, gather, implicit, flags);
 }
@@ -218,19 +221,24 @@ __device__ __forceinline__ void load_inplace(double (&f)[Q], const Fld &s, int x
 // Measured -3 % (exact, after the power-of-two arithmetic savings) and -5 %
 // (fast, propagate) on B200 (profiles/r01_summary.md): kept as an option,
 // not used.
-template <bool STREAM>
+// MODE: LD_NC (__ldg), LD_STREAM (nc + L1::no_allocate) or LD_COH
+// (ld.global.cg: L2, coherent with peer stores landing during the kernel).
+enum { LD_NC = 0, LD_STREAM = 1, LD_COH = 2 };
+template <int MODE>
 __device__ __forceinline__ void load_plain(double (&f)[Q], const SiteLaunch &L, int x, int y) {
     const char *sp = reinterpret_cast<const char *>(
         L.src.base + (long long)x * L.src.sx + (long long)y * L.src.sy);
 #pragma unroll
     for (int l = 0; l < Q; ++l) {
-        if constexpr (STREAM) {
+        const double *p = reinterpret_cast<const double *>(sp + L.soffb[l]);
+        if constexpr (MODE == LD_STREAM) {
             double v;
-            asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];"
-                         : "=d"(v) : "l"(sp + L.soffb[l]));
+            asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
             f[l] = v;
+        } else if constexpr (MODE == LD_COH) {
+            f[l] = __ldcg(p);
         } else {
-            f[l] = __ldg(reinterpret_cast<const double *>(sp + L.soffb[l]));
+            f[l] = __ldg(p);
         }
     }
 }
@@ -267,7 +275,7 @@ __device__ __forceinline__ void site_body(const SiteLaunch &L, int x, int y, boo
         const bool implicit = (L.flags & (TLB_F_WRAP_X | TLB_F_WRAP_Y | TLB_F_CLAMP_Y)) != 0;
         load_all(f, L.src, x, y, gather, implicit, L.flags);
     } else {
-        load_plain<false>(f, L, x, y);
+        load_plain<LD_NC>(f, L, x, y);
     }
     unsigned bits = 0;
     if (EDGE && (KIND == K_BC || KIND == K_FUSED)) {

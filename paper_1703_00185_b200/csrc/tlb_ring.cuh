@@ -84,11 +84,20 @@ struct TlbRing {
             return fail(TLB_ERR_CUDA, "%s: %s", #expr, tlbring::nccl().GetErrorString(_r)); \
     } while (0)
 
-// pack / unpack both X faces in one launch each
-__global__ void k_pack2(Fld f, FaceLines tp, FaceLines tm, int ymode, double *buf, int n_per) {
+// Payload layout per face: the face-plan lines, then one double holding the
+// sender's step number (the step tag of Fabric.send/recv, runtime.py:141-160):
+// a receiver at another step flags TLB_ST_PROTOCOL instead of consuming
+// halos of the wrong step.
+// pack / unpack both X faces in one launch each (stride = lines * NY + 1)
+__global__ void k_pack2(Fld f, FaceLines tp, FaceLines tm, int ymode, double *buf, int stride,
+                        double tag) {
     const int NY = f.Ly + 2 * f.Hy;
     const int k = blockIdx.y;
     const int y = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k == 0 && y == 0) {
+        buf[stride - 1] = tag;
+        buf[2 * stride - 1] = tag;
+    }
     if (y >= NY) return;
     const bool plus = k < tp.n;
     const int kk = plus ? k : k - tp.n;
@@ -97,15 +106,23 @@ __global__ void k_pack2(Fld f, FaceLines tp, FaceLines tm, int ymode, double *bu
     const int d = plus ? tp.d[kk] : tm.d[kk];
     const int col = plus ? f.Hx + f.Lx - d : f.Hx + d - 1;
     const int ys = ysrc_mode(y, f, ymode);
-    double *out = buf + (plus ? 0 : n_per);
+    double *out = buf + (plus ? 0 : stride);
     out[(long long)kk * NY + y] =
         f.base[(long long)l * f.sl + (long long)col * f.sx + (long long)ys * f.sy];
 }
 
-__global__ void k_unpack2(Fld f, FaceLines tp, FaceLines tm, const double *buf, int n_per) {
+__device__ __forceinline__ void check_tags(const double *a, const double *b, double expect,
+                                           TlbStatus *st, int step) {
+    if (st && expect >= 0.0 && (a[0] != expect || b[0] != expect))
+        report(st, TLB_ST_PROTOCOL, -1, -1, step);
+}
+
+__global__ void k_unpack2(Fld f, FaceLines tp, FaceLines tm, const double *buf, int stride,
+                          double expect, TlbStatus *st) {
     const int NY = f.Ly + 2 * f.Hy;
     const int k = blockIdx.y;
     const int y = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k == 0 && y == 0) check_tags(buf + stride - 1, buf + 2 * stride - 1, expect, st, (int)expect);
     if (y >= NY) return;
     const bool plus = k < tp.n;  // arrived travelling +x: from the left -> low-x halo
     const int kk = plus ? k : k - tp.n;
@@ -113,57 +130,76 @@ __global__ void k_unpack2(Fld f, FaceLines tp, FaceLines tm, const double *buf, 
     const int l = plus ? tp.l[kk] : tm.l[kk];
     const int d = plus ? tp.d[kk] : tm.d[kk];
     const int col = plus ? f.Hx - d : f.Hx + f.Lx - 1 + d;
-    const double *in = buf + (plus ? 0 : n_per);
+    const double *in = buf + (plus ? 0 : stride);
     f.base[(long long)l * f.sl + (long long)col * f.sx + (long long)y * f.sy] =
         in[(long long)kk * NY + y];
 }
 
-static int ring_pack(const TlbField *f, int ymode, double *sbuf, cudaStream_t s) {
+__global__ void k_tags_put(double *a, double *b, double tag) {
+    if (a) a[0] = tag;
+    if (b) b[0] = tag;
+}
+
+__global__ void k_tags_check(const double *a, const double *b, double expect, TlbStatus *st) {
+    if (st && expect >= 0.0 && ((a && a[0] != expect) || (b && b[0] != expect)))
+        report(st, TLB_ST_PROTOCOL, -1, -1, (int)expect);
+}
+
+static int ring_stride(const TlbField *f) { return (int)tlb_face_payload_len(f) + 1; }
+
+static int ring_pack(const TlbField *f, int ymode, double *sbuf, double tag, cudaStream_t s) {
     FaceLines tp = face_lines(1, 0), tm = face_lines(-1, 0);
     const int NY = f->Ly + 2 * f->Hy;
     dim3 grid((NY + 127) / 128, tp.n + tm.n);
-    k_pack2<<<grid, 128, 0, s>>>(mkfld(f), tp, tm, ymode, sbuf, tp.n * NY);
+    k_pack2<<<grid, 128, 0, s>>>(mkfld(f), tp, tm, ymode, sbuf, ring_stride(f), tag);
     return launch_check("ring pack");
 }
 
-static int ring_unpack(const TlbField *f, const double *rbuf, cudaStream_t s) {
+static int ring_unpack(const TlbField *f, const double *rbuf, double expect, TlbStatus *st,
+                       cudaStream_t s) {
     FaceLines tp = face_lines(1, 0), tm = face_lines(-1, 0);
     const int NY = f->Ly + 2 * f->Hy;
     dim3 grid((NY + 127) / 128, tp.n + tm.n);
-    k_unpack2<<<grid, 128, 0, s>>>(mkfld(f), tp, tm, rbuf, tp.n * NY);
+    k_unpack2<<<grid, 128, 0, s>>>(mkfld(f), tp, tm, rbuf, ring_stride(f), expect, st);
     return launch_check("ring unpack");
 }
 
 // Y faces (pbc_nc, runtime.py:248-267): rows of physical columns travel up
 // and down; the group order pairs each send with the matching receive even
-// when up == down (two ranks on a periodic Y ring).
-static int ring_exchange_y(TlbRing *r, const TlbField *f, cudaStream_t s) {
+// when up == down (two ranks on a periodic Y ring).  Each payload carries
+// the step tag after its lines (stride n + 1).
+static int ring_exchange_y(TlbRing *r, const TlbField *f, double tag, TlbStatus *st,
+                           cudaStream_t s) {
     auto &N = tlbring::nccl();
-    const size_t n = (size_t)tlb_face_payload_len_y(f);
-    double *s_up = r->ybuf, *s_dn = r->ybuf + n, *r_dn = r->ybuf + 2 * n, *r_up = r->ybuf + 3 * n;
+    const size_t n = (size_t)tlb_face_payload_len_y(f), m = n + 1;
+    double *s_up = r->ybuf, *s_dn = r->ybuf + m, *r_dn = r->ybuf + 2 * m, *r_up = r->ybuf + 3 * m;
     int e;
     if (r->up >= 0 && (e = tlb_pack_y(f, 1, s_up, s))) return e;
     if (r->down >= 0 && (e = tlb_pack_y(f, -1, s_dn, s))) return e;
+    k_tags_put<<<1, 1, 0, s>>>(r->up >= 0 ? s_up + n : nullptr, r->down >= 0 ? s_dn + n : nullptr,
+                               tag);
     TLB_NCCL_CHECK(N.GroupStart());
-    if (r->up >= 0) TLB_NCCL_CHECK(N.Send(s_up, n, ncclFloat64, r->up, r->comm, s));
-    if (r->down >= 0) TLB_NCCL_CHECK(N.Recv(r_dn, n, ncclFloat64, r->down, r->comm, s));
-    if (r->down >= 0) TLB_NCCL_CHECK(N.Send(s_dn, n, ncclFloat64, r->down, r->comm, s));
-    if (r->up >= 0) TLB_NCCL_CHECK(N.Recv(r_up, n, ncclFloat64, r->up, r->comm, s));
+    if (r->up >= 0) TLB_NCCL_CHECK(N.Send(s_up, m, ncclFloat64, r->up, r->comm, s));
+    if (r->down >= 0) TLB_NCCL_CHECK(N.Recv(r_dn, m, ncclFloat64, r->down, r->comm, s));
+    if (r->down >= 0) TLB_NCCL_CHECK(N.Send(s_dn, m, ncclFloat64, r->down, r->comm, s));
+    if (r->up >= 0) TLB_NCCL_CHECK(N.Recv(r_up, m, ncclFloat64, r->up, r->comm, s));
     TLB_NCCL_CHECK(N.GroupEnd());
+    k_tags_check<<<1, 1, 0, s>>>(r->down >= 0 ? r_dn + n : nullptr, r->up >= 0 ? r_up + n : nullptr,
+                                 tag, st);
     if (r->down >= 0 && (e = tlb_unpack_y(f, 1, r_dn, s))) return e;
     if (r->up >= 0 && (e = tlb_unpack_y(f, -1, r_up, s))) return e;
     return TLB_OK;
 }
 
-static int ring_exchange(TlbRing *r, size_t n_per, const double *sbuf, double *rbuf,
+static int ring_exchange(TlbRing *r, size_t stride, const double *sbuf, double *rbuf,
                          cudaStream_t s) {
     auto &N = tlbring::nccl();
     // data travelling +x goes to the right neighbour and arrives from the left
     TLB_NCCL_CHECK(N.GroupStart());
-    TLB_NCCL_CHECK(N.Send(sbuf, n_per, ncclFloat64, r->right, r->comm, s));
-    TLB_NCCL_CHECK(N.Recv(rbuf, n_per, ncclFloat64, r->left, r->comm, s));
-    TLB_NCCL_CHECK(N.Send(sbuf + n_per, n_per, ncclFloat64, r->left, r->comm, s));
-    TLB_NCCL_CHECK(N.Recv(rbuf + n_per, n_per, ncclFloat64, r->right, r->comm, s));
+    TLB_NCCL_CHECK(N.Send(sbuf, stride, ncclFloat64, r->right, r->comm, s));
+    TLB_NCCL_CHECK(N.Recv(rbuf, stride, ncclFloat64, r->left, r->comm, s));
+    TLB_NCCL_CHECK(N.Send(sbuf + stride, stride, ncclFloat64, r->left, r->comm, s));
+    TLB_NCCL_CHECK(N.Recv(rbuf + stride, stride, ncclFloat64, r->right, r->comm, s));
     TLB_NCCL_CHECK(N.GroupEnd());
     return TLB_OK;
 }
@@ -263,16 +299,15 @@ int tlb_ring_exchange(tlb_ring_t r, const TlbField *f, int ymode, double *sbuf, 
                       tlb_stream_t stream) {
     cudaStream_t s = (cudaStream_t)stream;
     int e;
-    if ((r->up >= 0 || r->down >= 0) && (e = ring_exchange_y(r, f, s))) return e;
-    if ((e = ring_pack(f, ymode, sbuf, s))) return e;
-    const size_t n_per = (size_t)tlb_face_payload_len(f);
-    if ((e = ring_exchange(r, n_per, sbuf, rbuf, s))) return e;
-    return ring_unpack(f, rbuf, s);
+    if ((r->up >= 0 || r->down >= 0) && (e = ring_exchange_y(r, f, -1.0, nullptr, s))) return e;
+    if ((e = ring_pack(f, ymode, sbuf, -1.0, s))) return e;
+    if ((e = ring_exchange(r, (size_t)ring_stride(f), sbuf, rbuf, s))) return e;
+    return ring_unpack(f, rbuf, -1.0, nullptr, s);
 }
 
 int tlb_ring_step(tlb_ring_t r, const TlbField *prv, const TlbField *nxt, const TlbParams *p,
                   int flags, TlbStatus *status, double *sbuf, double *rbuf,
-                  void *ev_bulk0, void *ev_bulk1, tlb_stream_t stream) {
+                  void *ev_bulk0, void *ev_bulk1, int64_t step_tag, tlb_stream_t stream) {
     int e;
     if ((e = check_stencil())) return e;
     if ((e = check_params(p))) return e;
@@ -289,10 +324,10 @@ int tlb_ring_step(tlb_ring_t r, const TlbField *prv, const TlbField *nxt, const 
     TLB_CUDA_CHECK(cudaEventRecord(r->ev_pack, s));
     TLB_CUDA_CHECK(cudaStreamWaitEvent(r->side, r->ev_pack, 0));
     // 2. Y faces first (2-D), then X faces carrying the Y halo rows
-    if (has_y && (e = ring_exchange_y(r, prv, r->side))) return e;
-    if ((e = ring_pack(prv, ymode, sbuf, r->side))) return e;
-    const size_t n_per = (size_t)tlb_face_payload_len(prv);
-    if ((e = ring_exchange(r, n_per, sbuf, rbuf, r->side))) return e;
+    const double tag = (double)step_tag;
+    if (has_y && (e = ring_exchange_y(r, prv, tag, status, r->side))) return e;
+    if ((e = ring_pack(prv, ymode, sbuf, tag, r->side))) return e;
+    if ((e = ring_exchange(r, (size_t)ring_stride(prv), sbuf, rbuf, r->side))) return e;
     // 3. bulk on the main stream, concurrent with the exchanges: all columns
     //    >= 3 from the X edges, all rows not within 3 of an exchanged Y edge
     if (ev_bulk0) TLB_CUDA_CHECK(cudaEventRecord((cudaEvent_t)ev_bulk0, s));
@@ -303,7 +338,7 @@ int tlb_ring_step(tlb_ring_t r, const TlbField *prv, const TlbField *nxt, const 
     }
     if (ev_bulk1) TLB_CUDA_CHECK(cudaEventRecord((cudaEvent_t)ev_bulk1, s));
     // 4. halos in, then the frame bands (one launch) on the side stream
-    if ((e = ring_unpack(prv, rbuf, r->side))) return e;
+    if ((e = ring_unpack(prv, rbuf, tag, status, r->side))) return e;
     {
         SiteLaunch L;
         memset(&L, 0, sizeof L);

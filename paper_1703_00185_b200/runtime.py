@@ -397,9 +397,10 @@ class RankWorker:
             if isinstance(fabric, DistFabric) and fabric.native and fabric.Np > 1:
                 import ctypes
                 self._ring = fabric.ring(self.device.index)
-                self.sbuf2 = torch.empty(2 * n, dtype=torch.float64, device=self.device)
-                self.rbuf2 = torch.empty(2 * n, dtype=torch.float64, device=self.device)
-                self.ybuf4 = torch.empty(4 * ny_, dtype=torch.float64, device=self.device)
+                # two X payloads (+ a step tag each), four Y payloads (ditto)
+                self.sbuf2 = torch.empty(2 * (n + 1), dtype=torch.float64, device=self.device)
+                self.rbuf2 = torch.empty(2 * (n + 1), dtype=torch.float64, device=self.device)
+                self.ybuf4 = torch.empty(4 * (ny_ + 1), dtype=torch.float64, device=self.device)
                 _lib.check(lib.tlb_ring_set_neighbors(
                     self._ring, nb["left"], nb["right"],
                     nb["up"] if self.ex_up else -1, nb["down"] if self.ex_down else -1,
@@ -416,10 +417,14 @@ class RankWorker:
             # exchanged direction.  "auto" takes it when it applies, else
             # the NCCL ring; "p2p" insists.
             order = params.eq_order if params.eq_order is not None else vs.eq_order
-            peer_ok = (self._ring is not None and (not self.x_self or self.y_exchange)
-                       and schedule == "overlapped" and vs.Q == 37 and order == 4
-                       and (self.x_self or tile.Lx >= 7)
-                       and (not self.y_exchange or tile.Ly >= 7))
+            # in-process ranks (Fabric) link their peers once all tiles exist
+            # (link_local_peers); one process per GPU maps them over CUDA IPC
+            self.peer_capable = ((not self.x_self or self.y_exchange)
+                                 and schedule == "overlapped" and vs.Q == 37 and order == 4
+                                 and (self.x_self or tile.Lx >= 7)
+                                 and (not self.y_exchange or tile.Ly >= 7))
+            peer_ok = self._ring is not None and self.peer_capable
+            self.exchange = exchange
             if exchange == "p2p" and not peer_ok and self._ring is not None:
                 raise ConfigurationError(
                     "exchange='p2p' needs D2Q37 order-4 tiles >= 7 sites across each "
@@ -498,11 +503,26 @@ class RankWorker:
             if ok:
                 lib.tlb_peer_destroy(hp)
             return
+        self._adopt_peer(hp, getattr(fabric, "timeout", None))
+        fabric.dist.barrier(group=fabric.group)
+
+    def _adopt_peer(self, hp, timeout):
+        """Start stepping through the peer object hp (buffer A = prv now)."""
+        torch = _lib.torch_cuda()
+        if timeout:
+            _lib.check(_lib.load().tlb_peer_set_timeout(hp, float(timeout)), "peer timeout")
         self._peer = hp
         self._bufA = self.prv.data.data_ptr()
         self._peer_step = 0
+        self._last_tag = None
         self._primed = False
-        fabric.dist.barrier(group=fabric.group)
+        if self.debug_poison:
+            # both buffers' halos start poisoned; afterwards every peer step
+            # re-poisons prv's halos once its border blocks have read them
+            # (TLB_F_POISON_HALOS), before any neighbour may store into them
+            self._poison_halos(self.prv)
+            self._poison_halos(self.nxt)
+        torch.cuda.synchronize(self.device)
 
     # the eight directions of csrc/tlb_peer.cuh: (dx, dy)
     _PEER_DIRS = ((-1, 0), (1, 0), (0, -1), (0, 1), (-1, -1), (1, -1), (-1, 1), (1, 1))
@@ -814,7 +834,7 @@ class RankWorker:
         self._hy = self._hx = None
         self._bulk_timed = False
         self._rec(ev, 0)
-        if self.debug_poison:
+        if self.debug_poison and self._peer is None:
             self._poison_halos(self.prv)
         if self.schedule == "staged":
             # the reference's order: wall extension, Y halos, X halos
@@ -832,19 +852,26 @@ class RankWorker:
         self._flags_now = flags
         if self._peer is not None:
             if not self._primed:
-                # fill prv's halos once through NCCL; afterwards every step's
-                # border threads write the neighbours' halos directly
-                self._check(lib.tlb_ring_exchange(
-                    self._ring, field_desc(self.prv), self._ymode(), self.sbuf2.data_ptr(),
-                    self.rbuf2.data_ptr(), self._sp()), "ring exchange")
+                # fill prv's halos once: the border sites push their values
+                # into the neighbours' halos as if step_no-1 had just run;
+                # afterwards every step's border threads write them directly
+                prv_index = 0 if self.prv.data.data_ptr() == self._bufA else 1
+                self._check(lib.tlb_peer_prime(
+                    self._peer, field_desc(self.prv), prv_index, self.tparams, st,
+                    self.mailbox.data_ptr(), self._peer_step, step_no - 1, self._sp()),
+                    "peer prime")
+                self._peer_step += 1
+                self._last_tag = step_no - 1
                 self._primed = True
             nxt_index = 0 if self.nxt.data.data_ptr() == self._bufA else 1
+            pflags = flags | (_lib.F_POISON_HALOS if self.debug_poison else 0)
             self._rec(ev, 1)
             self._check(lib.tlb_peer_step(
                 self._peer, field_desc(self.prv), field_desc(self.nxt), nxt_index,
-                self.tparams, flags, st, self.mailbox.data_ptr(), self._peer_step,
-                self._sp()), "peer step")
+                self.tparams, pflags, st, self.mailbox.data_ptr(), self._peer_step,
+                step_no, int(self._last_tag == step_no - 1), self._sp()), "peer step")
             self._peer_step += 1
+            self._last_tag = step_no
             self._rec(ev, 2)
             self._bulk_timed = True
             return
@@ -855,7 +882,7 @@ class RankWorker:
                 self._ring, field_desc(self.prv), field_desc(self.nxt), self.tparams,
                 flags & ~_lib.F_WRAP_X, st, self.sbuf2.data_ptr(), self.rbuf2.data_ptr(),
                 ev[1].cuda_event if ev else None, ev[2].cuda_event if ev else None,
-                self._sp()), "ring step")
+                step_no, self._sp()), "ring step")
             self._bulk_timed = True
             return
         if self.x_self and not self.y_exchange:
@@ -1011,6 +1038,9 @@ class RankWorker:
             self._status_ring.zero_()
         if err is not None and raise_errors:
             step, s = err
+            if s.flags & _lib.ST_PROTOCOL:
+                raise ProtocolError(f"rank {self.tile.rank} step {step}: a neighbour's halo "
+                                    "carries another step's tag")
             if s.flags & _lib.ST_PEER_TIMEOUT:
                 raise DeadlockError(f"rank {self.tile.rank} step {step}: a ring neighbour did "
                                     "not publish its step (peer-memory exchange)",
@@ -1053,3 +1083,58 @@ class RankWorker:
             self.prv.pops[:, g.phys_x, g.phys_y].copy_(src, non_blocking=True)
             if src.is_cuda and src.device == self.device:
                 src.record_stream(self.stream)
+
+
+def link_local_peers(workers, strict=False):
+    """Peer stores for in-process ranks (the Fabric's simulated ranks,
+    runtime.py:116-160): every tile's step kernel stores its border
+    populations straight into its neighbours' halos and publishes the step
+    through a device mailbox (csrc/tlb_peer.cuh) -- the kernel of one process
+    per GPU, with plain device pointers instead of CUDA IPC.  `workers` must
+    hold every rank.  Returns True when linked; with strict=False the ranks
+    keep the Fabric exchange when the peer step does not apply."""
+    import ctypes
+    torch = _lib.torch_cuda()
+    by_rank = {w.tile.rank: w for w in workers}
+    ok = (len(workers) > 1 and all(w.peer_capable for w in workers)
+          and len(by_rank) == workers[0].Np and all(w._peer is None for w in workers))
+    if not ok:
+        if strict:
+            raise ConfigurationError(
+                "exchange='p2p' needs D2Q37 order-4 tiles >= 7 sites across each exchanged "
+                "direction with the overlapped schedule, and every rank in this process")
+        return False
+    lib = _lib.load()
+    for w in workers:
+        with torch.cuda.device(w.device):
+            w.mailbox = torch.zeros(16, dtype=torch.int64, device=w.device)
+    for w in workers:
+        torch.cuda.synchronize(w.device)
+    handles = []
+    try:
+        for w in workers:
+            ptrs = (ctypes.c_void_p * 24)()
+            present = (ctypes.c_int * 8)()
+            for d, r in enumerate(w._peer_neighbours()):
+                if r is None:
+                    continue
+                nb = by_rank[r]
+                present[d] = 1
+                ptrs[3 * d] = nb.prv.data.data_ptr()      # buffer A = prv now, on every rank
+                ptrs[3 * d + 1] = nb.nxt.data.data_ptr()
+                ptrs[3 * d + 2] = nb.mailbox.data_ptr()
+            hp = ctypes.c_void_p()
+            _lib.check(lib.tlb_peer_create_local(w.device.index, ptrs, present,
+                                                 ctypes.byref(hp)), "peer create (local)")
+            handles.append(hp)
+    except ThermoLBError:
+        for hp in handles:
+            lib.tlb_peer_destroy(hp)
+        if strict:
+            raise
+        return False
+    for w, hp in zip(workers, handles):
+        with torch.cuda.device(w.device):
+            w._adopt_peer(hp, getattr(w.fabric, "timeout", None))
+        w.exchange_mode = "p2p"
+    return True

@@ -53,6 +53,26 @@ def main():
         cases.append(((2, world // 2), "overlapped", "p2p", True))
         cases.append(((2, world // 2), "overlapped", "nccl", True))
     ok = True
+    # snapshots (reduced to rho, u, T on the device and gathered on rank 0,
+    # reference sim.py:89-90, 119-125) and NaN-poisoned halos (runtime.py:
+    # 288-294) on both native transports
+    for exchange in ("p2p", "nccl"):
+        res = tl.run(tl.SimConfig(Lx=Lx, Ly=Ly, Np=world, steps=steps, params=p,
+                                  init="rayleigh-taylor", exchange=exchange,
+                                  snapshot_every=3, debug_poison=True))
+        if rank == 0:
+            same = np.array_equal(res.populations, want)
+            snaps_ok = [s for s, _ in res.snapshots] == [3, 6, 9]
+            for s_, m in res.snapshots:
+                ref_s, _ = O.run(f0, s_, p6)
+                rho, ux, uy, T = O.moments(ref_s)
+                snaps_ok &= all(np.array_equal(a, b) for a, b in
+                                ((m.rho, rho), (m.ux, ux), (m.uy, uy), (m.T, T)))
+            rho, ux, uy, T = O.moments(want)
+            macro_ok = np.array_equal(res.macro.rho, rho) and np.array_equal(res.macro.T, T)
+            print(f"snapshots+poison exchange={exchange} world={world} ok={same} "
+                  f"snapshots={snaps_ok} macro={macro_ok}", flush=True)
+            ok &= same and snaps_ok and macro_ok
     for tiling, schedule, exchange, periodic in cases:
         for arith in (("exact", "fast") if exchange == "p2p" else ("exact",)):
             pp = tl.PhysicsParams(tau=p.tau, gx=p.gx, gy=p.gy, Twall_top=p.Twall_top,
