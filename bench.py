@@ -35,33 +35,66 @@ BYTES_SITE = 592          # fused step: 37 x 8 B read + 37 x 8 B written
 TILE_LX, TILE_LY = 1920, 2048
 
 
-def ncu_traffic(arith, layout="column"):
-    """dram__bytes_read.sum + dram__bytes_write.sum (GB) of the fused step
-    kernel from the committed `ncu --set full` capture of the same storage
-    layout (profiles/*ncu*_<layout>_raw.csv), or None."""
+_SASS = None
+
+
+def sass_hash(kernel):
+    """sha256 (16 hex) of the SASS of the libtlb.so function whose demangled
+    name contains `kernel` (cuobjdump), or None."""
+    global _SASS
+    import hashlib
+    import re
+    if _SASS is None:
+        lib = os.path.join(ROOT, "paper_1703_00185_b200", "libtlb.so")
+        try:
+            txt = subprocess.run(["cuobjdump", "-sass", lib], capture_output=True, text=True,
+                                 timeout=120).stdout
+            dem = subprocess.run(["cu++filt"], input="\n".join(
+                re.findall(r"Function : (\S+)", txt)), capture_output=True, text=True,
+                timeout=60).stdout.split("\n")
+        except (OSError, subprocess.SubprocessError):
+            _SASS = {}
+            return None
+        blocks = re.split(r"\n\s*Function : \S+", txt)[1:]
+        _SASS = dict(zip(dem, blocks))
+    for name, body in _SASS.items():
+        if kernel in name.replace("(bool)", "").replace("(int)", ""):
+            # drop addresses and encodings: the instruction text only
+            ins = re.findall(r"/\*[0-9a-f]{4,}\*/\s+([^;]*;)", body)
+            return hashlib.sha256("\n".join(ins).encode()).hexdigest()[:16]
+    return None
+
+
+def ncu_traffic(kernel, layout="column"):
+    """dram__bytes_read.sum + dram__bytes_write.sum (GB) of `kernel` from the
+    committed `ncu --set full` capture of the same storage layout
+    (profiles/*ncu*_<layout>_raw*.csv) -- only from a capture whose sidecar
+    <csv>.sass records the SASS hash of the kernel in THIS libtlb.so."""
     import csv
     import glob
-    want = "k_site<3, %d, 4, 0, 4" % (1 if arith == "exact" else 0)
+    want_hash = sass_hash(kernel)
     paths = sorted(glob.glob(os.path.join(ROOT, "profiles", f"*ncu*_{layout}_raw*.csv")),
                    reverse=True)
     for path in paths:
         try:
+            with open(path + ".sass") as fh:
+                tags = dict(line.strip().split(" ", 1) for line in fh if " " in line)
             rows = list(csv.reader(open(path)))
-        except OSError:
+        except (OSError, ValueError):
             continue
-        if not rows:
+        if not rows or want_hash is None or tags.get(kernel) != want_hash:
             continue
         hdr = rows[0]
         for r in rows[2:]:
             d = dict(zip(hdr, r))
-            if want in d.get("Kernel Name", ""):
+            if kernel in d.get("Kernel Name", "").replace("(bool)", "").replace("(int)", ""):
                 try:
-                    # ncu reports dram__bytes_* in GB in the raw page
                     return round(float(d["dram__bytes_read.sum"]) +
-                                 float(d["dram__bytes_write.sum"]), 4), os.path.basename(path)
+                                 float(d["dram__bytes_write.sum"]), 4), \
+                        f"{os.path.basename(path)} (SASS {want_hash})"
                 except (KeyError, ValueError):
                     continue
-    return None, None
+    return None, f"no capture of this binary's {kernel} (SASS {want_hash})"
 
 
 def peaks():
@@ -162,10 +195,7 @@ class ClockSampler:
 
 # ------------------------------------------------------------ CPU oracle --
 
-def cpu_oracle_rate(seconds, steps=None, warmup=0, Lx=240, Ly=TILE_LY):
-    """C oracle (oracle/tlb_oracle.c, bitwise = the reference) with all host
-    threads on an RT Lx x Ly sample lattice.  Returns (MLUPS, threads,
-    steps, sample description)."""
+def _oracle_setup():
     from oracle import oracle as O
     import paper_1703_00185_b200 as tl
     O.build()
@@ -174,37 +204,54 @@ def cpu_oracle_rate(seconds, steps=None, warmup=0, Lx=240, Ly=TILE_LY):
     nthreads = len(os.sched_getaffinity(0))
     O.threads(nthreads)
     p6 = O.params6(0.8, 0.0, -1e-5, 1.0, 0.9 * vs.cs2, 1.1 * vs.cs2)
+    return O, vs, nthreads, p6
+
+
+def cpu_oracle_rate(seconds=None, steps=None, warmup=2, Lx=TILE_LX, Ly=TILE_LY):
+    """The C oracle (oracle/tlb_oracle.c, bitwise = the reference) with all
+    host threads on the RT Lx x Ly lattice itself: `warmup` untimed steps
+    (OpenMP pool up, buffers faulted in), then `steps` steps -- or as many as
+    fit in `seconds`, sized from a one-step probe -- timed inside the C
+    library.  Returns (MLUPS, threads, steps, seconds, description)."""
+    O, vs, nthreads, p6 = _oracle_setup()
     f0 = O.equilibrium(*O.rayleigh_taylor_macro(Lx, Ly, vs.cs2))
-    t1 = time.perf_counter()
-    f0, _ = O.run(f0, max(warmup, 1), p6)     # warm-up (also sizes the sample)
-    per_step = (time.perf_counter() - t1) / max(warmup, 1)
-    done = steps if steps is not None else max(3, int(seconds / per_step))
-    t0 = time.perf_counter()
-    f, _ = O.run(f0, done, p6)                # one call: buffers allocated once
-    el = time.perf_counter() - t0
-    return (Lx * Ly * done / el / 1e6, nthreads, done,
-            f"RT {Lx}x{Ly} sample lattice (walls, periodic X), {done} steps, "
-            f"{nthreads} threads, {el:.1f} s")
+    if steps is None:
+        _, one = O.run_timed(f0, 1, 1, p6)
+        steps = max(3, int(seconds / max(one, 1e-6)))
+    _, el = O.run_timed(f0, warmup, steps, p6)
+    return (Lx * Ly * steps / el / 1e6, nthreads, steps, el,
+            f"RT {Lx}x{Ly} (walls, periodic X), {warmup} untimed + {steps} timed steps, "
+            f"{nthreads} threads, {el:.2f} s")
 
 
 def reference_arm(args, rank, world):
+    """--impl reference: the reference algorithm on the host CPU (the C
+    oracle, every host thread) on the workload of the GPU arm's config --
+    configs[1]/[2]: the whole (1920*N) x 2048 lattice, W untimed + K timed
+    steps; configs[3] (strong, 8192x16384 = 79.5 GB of host buffers): a
+    1024x16384 column band of it, the per-site work being identical."""
     if rank != 0:
         return 0
-    mlups, nthreads, done, sample = cpu_oracle_rate(None, steps=args.steps, warmup=args.warmup)
     if args.strong:
         Lx, Ly = 8192, 16384
+        sLx, sLy = 1024, 16384
         workload = f"D2Q37 RT {Lx}x{Ly} (strong scaling, {world} tiles)"
     else:
         Lx, Ly = args.Lx * world, args.Ly
-        workload = f"D2Q37 RT {Lx}x{Ly} (1-D X tiles of {args.Lx}x{args.Ly})"
+        sLx, sLy = Lx, Ly
+        workload = (f"D2Q37 RT {Lx}x{Ly} on 1 B200 (BASELINE configs[1])" if world == 1 else
+                    f"D2Q37 RT {Lx}x{Ly} (1-D X tiles of {args.Lx}x{args.Ly})")
+    mlups, nthreads, done, el, sample = cpu_oracle_rate(steps=args.steps, warmup=args.warmup,
+                                                        Lx=sLx, Ly=sLy)
+    ms_step = el / done * 1e3 * (Lx * Ly) / (sLx * sLy)
     line = {
         "impl": "reference", "metric": METRIC, "value": round(mlups, 4), "unit": "MLUPS",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        # the workload's step at the sampled site rate
-        "ms_per_step": round(Lx * Ly / (mlups * 1e6) * 1e3, 3),
+        "ms_per_step": round(ms_step, 3),
         "higher_is_better": True, "scaling": "strong" if args.strong else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (Rayleigh-Taylor init)",
-        "config": {"workload": workload, "sample": sample},
+        "config": {"workload": workload, "sample": sample,
+                   "same_lattice": (sLx, sLy) == (Lx, Ly)},
         "gflops_fp64": round(mlups * FLOP_SITE / 1e3, 3),
         "cpu_baseline": {"value": round(mlups, 4), "unit": "MLUPS", "cores": nthreads,
                          "kind": "port", "sample": sample},
@@ -260,9 +307,18 @@ def gpu_arm(args, rank, world, local_rank):
         if dist is not None:
             dist.barrier(device_ids=[local_rank])
 
+    # one tile (N=1): two steps per launch where it applies (temporal
+    # blocking, csrc/tb2.cu; RankWorker.pairable) -- run()'s own path
     def run_steps(n, s0=0):
-        for s in range(s0, s0 + n):
-            w.step(s)
+        pair = world == 1 and w.pairable()
+        s = s0
+        while s < s0 + n:
+            if pair and s + 1 < s0 + n:
+                w.step_pair(s)
+                s += 2
+            else:
+                w.step(s)
+                s += 1
 
     # warm-up (also sizes the clock pre-load identically on every rank: each
     # rank must run exactly the same number of ring steps)
@@ -321,7 +377,11 @@ def gpu_arm(args, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     metrics = w.metrics
-    bulk_ms = ([ms / args.steps] if world == 1 else
+    pair = world == 1 and w.pairable()
+    launches = args.steps // 2 + args.steps % 2 if pair else args.steps
+    # N=1: the region holds only the step launches: per-launch time = region
+    # / launches (a two-step launch counts as two steps' worth)
+    bulk_ms = ([ms * (2.0 if pair else 1.0) / args.steps] if world == 1 else
                [m["t_bulk"] * 1e3 for m in metrics if m["t_bulk"] == m["t_bulk"]])
     sites = Lx * Ly
     mlups = sites * args.steps / (ms * 1e-3) / 1e6
@@ -381,7 +441,10 @@ def gpu_arm(args, rank, world, local_rank):
                             else "<=1e-12 relative (tests/test_gpu_parity.py)")}
 
     w.timing = "sampled"
-    traffic, traffic_src = ncu_traffic(args.arith, args.layout)
+    kname = ("k_tb2<%d, 64, 2, 2>" % (1 if args.arith == "exact" else 0) if pair else
+             "k_site<3, %d, 4, 0, 4>" % (1 if args.arith == "exact" else 0) if world == 1 else
+             "k_peer_step<%d, 0>" % (1 if args.arith == "exact" else 0))
+    traffic, traffic_src = ncu_traffic(kname, args.layout)
     out = None
     if rank == 0:
         lib = _lib.load()
@@ -390,7 +453,11 @@ def gpu_arm(args, rank, world, local_rank):
         if args.probe:
             _lib.check(lib.tlb_bench_dfma(200000, ctypes.byref(fp), _lib.stream_ptr()), "dfma")
         fp64_peak = fp.value / 1e12 if args.probe else float("nan")
-        kern_tflops = (FLOP_SITE * kern_sites) / (kern_ms * 1e-3) / 1e12
+        steps_per_launch = 2 if pair else 1
+        kern_tflops = (steps_per_launch * FLOP_SITE * kern_sites) / (kern_ms * 1e-3) / 1e12
+        # nominal FP64 peak at the measured SM clock: 148 SMs x 64 DFMA/clk x 2
+        sm_mhz = (clocks or {}).get("sm_mhz") or 1965.0
+        nominal_tf = 148 * 64 * 2 * sm_mhz * 1e6 / 1e12
         split = split_kernels(w, tl, _lib, field_desc, torch) if args.split else None
         out = {
             "metric": METRIC, "value": round(mlups, 3), "unit": "MLUPS",
@@ -417,16 +484,24 @@ def gpu_arm(args, rank, world, local_rank):
                          "traffic": traffic, "traffic_unit": "GB per launch (ncu dram read+write)",
                          "traffic_source": traffic_src,
                          "algorithmic_bytes_per_launch_GB": round(BYTES_SITE * kern_sites / 1e9, 4),
-                         "kernel": "k_site<FUSED> (propagate+bc+collide)",
-                         "bytes_per_site": BYTES_SITE, "sites_per_launch": kern_sites,
+                         "kernel": (kname + " (TWO steps per launch: propagate+bc+collide "
+                                    "twice, the intermediate state in shared memory)") if pair
+                         else kname + " (propagate+bc+collide)",
+                         "steps_per_launch": steps_per_launch,
+                         "bytes_per_site": BYTES_SITE,
+                         "bytes_per_site_update": BYTES_SITE // steps_per_launch,
+                         "sites_per_launch": kern_sites,
                          "avg_launch_ms": round(kern_ms, 5), "peak_source": peak_src,
-                         "launch_timing": ("CUDA events around the K timed launches / K "
-                                           "(one fused launch per step)" if world == 1 else
-                                           "CUDA event pairs on sampled steps, bulk kernel"),
+                         "launch_timing": ("CUDA events around the K timed steps / launches "
+                                           "(only step launches in the region)" if world == 1
+                                           else "CUDA event pairs on sampled steps, bulk kernel"),
                          "fp64": {"achieved_tflops": round(kern_tflops, 3),
+                                  "flops_per_site_update": FLOP_SITE,
+                                  "count": "algorithmic (reference expression tree)",
+                                  "peak_tflops_nominal_at_clock": round(nominal_tf, 3),
+                                  "frac_nominal": round(kern_tflops / nominal_tf, 4),
                                   "peak_tflops_measured_dfma": round(fp64_peak, 3),
-                                  "frac": round(kern_tflops / fp64_peak, 4),
-                                  "flops_per_site": FLOP_SITE}},
+                                  "frac": round(kern_tflops / fp64_peak, 4)}},
             "clocks": clocks,
             "energy": ({"uJ_per_site_update": round(clocks["power_w_median"] * world /
                                                     (mlups * 1e6) * 1e6, 5),
@@ -437,7 +512,8 @@ def gpu_arm(args, rank, world, local_rank):
             "host_enqueue_ms_per_step": round(host_ms, 4),
             # our kernels per step: the fused step (N=1, or p2p: halo stores
             # fused in); NCCL ring: pack, bulk, unpack, border (+ NCCL's own)
-            "gpu_launches": args.steps * (1 if w.exchange_mode in ("self", "p2p") else 4),
+            "gpu_launches": (launches if world == 1 else
+                             args.steps * (1 if w.exchange_mode == "p2p" else 4)),
         }
         if split:
             out["split"] = split
@@ -447,11 +523,12 @@ def gpu_arm(args, rank, world, local_rank):
         if other:
             out["other_arith"] = other
     # e2e through the public API with host buffers
-    e2e = e2e_run(args, w, tl, torch, dist, local_rank, Lx_tile, Ly_tile) if args.e2e else None
+    e2e = (e2e_run(args, w, tl, torch, dist, local_rank, Lx_tile, Ly_tile, run_steps,
+                   ms / args.steps) if args.e2e else None)
     if rank == 0:
         out["e2e"] = e2e
         if world == 1 and args.cpu_seconds > 0:
-            mlups_cpu, nthreads, done, sample = cpu_oracle_rate(args.cpu_seconds)
+            mlups_cpu, nthreads, done, _, sample = cpu_oracle_rate(args.cpu_seconds)
             out["cpu_baseline"] = {"value": round(mlups_cpu, 4), "unit": "MLUPS",
                                    "cores": nthreads, "kind": "port", "sample": sample}
         emit(out)
@@ -469,7 +546,27 @@ def _gpu_index(local_rank):
     return local_rank
 
 
-def e2e_run(args, w, tl, torch, dist, local_rank, Lx_tile, Ly):
+def pcie_gbs(torch, dev, nbytes=1 << 30):
+    """Measured pinned host<->device copy bandwidth (GB/s), best of 3 each way."""
+    h = torch.empty(nbytes // 8, dtype=torch.float64, pin_memory=True)
+    d = torch.empty(nbytes // 8, dtype=torch.float64, device=dev)
+    out = {}
+    for name, (dst, src) in (("h2d", (d, h)), ("d2h", (h, d))):
+        best = 1e9
+        for _ in range(3):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            dst.copy_(src, non_blocking=True)
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        out[name] = nbytes / (best * 1e-3) / 1e9
+    del h, d
+    return out
+
+
+def e2e_run(args, w, tl, torch, dist, local_rank, Lx_tile, Ly, run_steps=None,
+            device_ms_per_step=None):
     """K steps end to end through the public API with host buffers.
 
     Headline (`value`): what `run()` does (sim.py): the initial macroscopic
@@ -501,8 +598,11 @@ def e2e_run(args, w, tl, torch, dist, local_rank, Lx_tile, Ly):
             w.load_block(tl.equilibrium(*ts, vs))
         else:
             w.load_block(host_in)
-        for s in range(steps):
-            w.step(s0 + s)
+        if run_steps is not None:
+            run_steps(steps, s0)
+        else:
+            for s in range(steps):
+                w.step(s0 + s)
         with torch.cuda.stream(w.stream):
             host_out.copy_(w.physical_block(), non_blocking=True)
         negatives = [m["negatives"] for m in w.metrics]  # D2H of per-step results
@@ -525,12 +625,29 @@ def e2e_run(args, w, tl, torch, dist, local_rank, Lx_tile, Ly):
     w.collect()
     v_pop, _ = timed(False, 10_000_000)
     v_mac, negatives = timed(True, 20_000_000)
+    bw = pcie_gbs(torch, w.device)
+    roof = None
+    if device_ms_per_step:
+        # the e2e bound: K device steps + the declared copies at the measured
+        # PCIe rates (per rank; every rank copies its own tile)
+        per = 1.0 / world
+        ideal_s = (args.steps * device_ms_per_step * 1e-3 +
+                   macro_bytes * per / (bw["h2d"] * 1e9) +
+                   (pops_bytes + metric_bytes) * per / (bw["d2h"] * 1e9))
+        ideal = Lx_tile * Ly * world * args.steps / ideal_s / 1e6
+        roof = {"bound": "pcie + device steps", "pcie_h2d_gbs": round(bw["h2d"], 1),
+                "pcie_d2h_gbs": round(bw["d2h"], 1), "ideal_mlups": round(ideal, 1),
+                "frac": round(v_mac / ideal, 4),
+                "note": "ideal = K x device ms/step + declared H2D/D2H bytes at the measured "
+                        "pinned copy bandwidth; at K=%d the %.2f GB final-state D2H dominates"
+                        % (args.steps, pops_bytes * per / 1e9)}
     return {"value": round(v_mac, 3), "unit": "MLUPS",
             "h2d_bytes_per_step": int(macro_bytes / args.steps),
             "d2h_bytes_per_step": int((pops_bytes + metric_bytes) / args.steps),
+            "roofline": roof,
             "note": "as run(): pinned host (rho,ux,uy,T) -> HBM -> device equilibrium, K steps "
-                    "via RankWorker.step, final populations + per-step negatives -> host; "
-                    "wall clock, max over ranks",
+                    "through RankWorker (two steps per launch on one tile), final populations "
+                    "+ per-step negatives -> host; wall clock, max over ranks",
             "populations_in": {"value": round(v_pop, 3), "unit": "MLUPS",
                                "h2d_bytes_per_step": int(pops_bytes / args.steps),
                                "d2h_bytes_per_step": int((pops_bytes + metric_bytes)
@@ -555,7 +672,10 @@ def split_kernels(w, tl, _lib, field_desc, torch):
         "bc": lambda: lib.tlb_bc(nxt, tp, 1, 1, g.Hx, g.Hx + g.Lx, st, sp),
         "collide": lambda: lib.tlb_collide(nxt, nxt, full, tp, 0, st, sp),
         "fused": lambda: lib.tlb_fused(prv, nxt, full, tp, flags_fused, st, sp),
+        # two whole steps per launch (temporal blocking): per-step figures below
+        "two_step": lambda: lib.tlb_step2_self(prv, nxt, tp, 1, 0, 0, st, st2, 0, sp),
     }
+    st2 = w._status_ring[1].data_ptr()
     res = {}
     sites = g.Lx * g.Ly
     for name, fn in ops.items():
@@ -570,13 +690,20 @@ def split_kernels(w, tl, _lib, field_desc, torch):
             ts.append(a.elapsed_time(b))
         msv = float(np.median(ts[1:]))
         r = {"ms": round(msv, 4)}
+        if name == "two_step":      # per step of the pair; 296 B/site per step
+            r = {"ms_per_launch": round(msv, 4), "ms": round(msv / 2, 4),
+                 "GBps": round(BYTES_SITE * sites / (msv * 1e-3) / 1e9, 1),
+                 "mlups": round(2 * sites / (msv * 1e-3) / 1e6, 1),
+                 "gflops": round(2 * FLOP_SITE * sites / (msv * 1e-3) / 1e9, 1)}
+            res[name] = r
+            continue
         if name == "bc":
             r["gflops"] = round(FLOP_WALL_SITE * 6 * g.Lx / (msv * 1e-3) / 1e9, 1)
             r["GBps"] = round(BYTES_SITE * 6 * g.Lx / (msv * 1e-3) / 1e9, 1)
         else:
             r["GBps"] = round(BYTES_SITE * sites / (msv * 1e-3) / 1e9, 1)
             r["mlups"] = round(sites / (msv * 1e-3) / 1e6, 1)
-            if name in ("collide", "fused"):
+            if name in ("collide", "fused", "two_step"):
                 r["gflops"] = round(FLOP_SITE * sites / (msv * 1e-3) / 1e9, 1)
         res[name] = r
     w.collect(raise_errors=False)

@@ -151,6 +151,16 @@ int tlb_step_self(const TlbField *prv, const TlbField *nxt,
                   const TlbParams *p, int walls, int periodic_y,
                   int count_neg, TlbStatus *status, tlb_stream_t stream);
 
+/* TWO whole time steps of such a rank in one launch (temporal blocking,
+ * csrc/tb2.cu): prv -> nxt after steps `step` and `step`+1, the intermediate
+ * state kept in shared memory.  Bitwise equal to two tlb_step_self calls;
+ * status1/status2 receive the per-step failures and negative counts.
+ * D2Q37 order 4, tiles of at least 8x8 (else TLB_ERR_UNSUPPORTED). */
+int tlb_step2_self(const TlbField *prv, const TlbField *nxt,
+                   const TlbParams *p, int walls, int periodic_y,
+                   int count_neg, TlbStatus *status1, TlbStatus *status2,
+                   int step, tlb_stream_t stream);
+
 /* moments               replaces kernels.moments, kernels.py:41-71.
  * Outputs are (nx, ny) arrays with row stride ld (elements). */
 int tlb_moments(const TlbField *f, TlbRegion r, double *rho, double *ux,
@@ -319,6 +329,9 @@ int tlb_pgm_image(const double *v, int64_t nx, int64_t ny, int64_t ld,
  * __launch_bounds__ minimum CTAs/SM of the fused kernel (1 = compiler's
  * choice, 4 = default, 5). */
 #define TLB_TUNE_MINBLOCKS 1
+#define TLB_TUNE_TB2_CFG 2   /* two-step kernel shape: 0 = 128 rows x 2 columns, 1 CTA/SM;
+                                1 = 64 x 2, 2 CTAs/SM; 2 = 96 x 2, 1 CTA/SM */
+#define TLB_TUNE_TB2_RUN 3   /* two-step kernel: columns per work item (default 96) */
 int tlb_set_tuning(int key, int value);
 
 /* Diagnostics: measured FP64 FMA throughput of this GPU (flop/s, 2 per

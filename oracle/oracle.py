@@ -56,6 +56,8 @@ def lib():
                                ctypes.c_int, ctypes.POINTER(_I64)]
         L.orc_run.argtypes = [_P, _P, _I64, _I64, _I64, _I64, ctypes.c_int, _P,
                               ctypes.c_int, ctypes.POINTER(_I64)]
+        L.orc_run_timed.argtypes = [_P, _P, _I64, _I64, _I64, _I64, _I64, ctypes.c_int, _P,
+                                    ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
         L.orc_set_threads.argtypes = [ctypes.c_int]
         _lib = L
     return _lib
@@ -198,6 +200,18 @@ def run(f0, steps, p6, H=3, ymode="walls", order=4, nthreads=None):
                          _ptr(p6), order,
                          neg.ctypes.data_as(ctypes.POINTER(_I64))))
     return out, neg[:steps]
+
+
+def run_timed(f0, warmup, steps, p6, H=3, ymode="walls", order=4):
+    """bench.py's CPU leg: `warmup` untimed steps, then `steps` steps timed
+    inside the C library (monotonic clock).  Returns (final block, seconds)."""
+    f0 = np.ascontiguousarray(f0, dtype=np.float64)
+    _, Lx, Ly = f0.shape
+    out = np.empty_like(f0)
+    sec = ctypes.c_double(0.0)
+    _check(lib().orc_run_timed(_ptr(f0), _ptr(out), Lx, Ly, H, warmup, steps, YMODES[ymode],
+                               _ptr(p6), order, ctypes.byref(sec)))
+    return out, sec.value
 
 
 # ---- initial conditions (numpy restatement of init.py) ---------------------

@@ -19,10 +19,12 @@
  * Storage is the reference's canonical SoA (Q, NX, NY) view: element
  * (l, x, y) lives at l*NX*NY + x*NY + y (geometry.py:68-74).
  */
+#define _POSIX_C_SOURCE 199309L  /* clock_gettime (orc_run_timed) */
 #include <math.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+#include <time.h>
 #ifdef _OPENMP
 #include <omp.h>
 #endif
@@ -387,6 +389,43 @@ int orc_run(const double *f_in, double *f_out, int64_t Lx, int64_t Ly,
                      negatives ? negatives + s : NULL);
         double *t = a; a = b; b = t;
     }
+    for (int l = 0; l < Q; ++l)
+        for (int64_t x = 0; x < Lx; ++x)
+            memcpy(f_out + (l * Lx + x) * Ly, a + l * plane + (x + H) * g.NY + H,
+                   sizeof(double) * Ly);
+    free(a);
+    free(b);
+    return e;
+}
+
+/* Benchmark leg of bench.py (cpu_baseline / --impl reference): orc_run with
+ * `warmup` untimed steps first (OpenMP pool started, both buffers faulted
+ * in), then `steps` steps timed with CLOCK_MONOTONIC. */
+int orc_run_timed(const double *f_in, double *f_out, int64_t Lx, int64_t Ly,
+                  int64_t H, int64_t warmup, int64_t steps, int ymode,
+                  const double *params6, int order, double *seconds) {
+    Geom g = mkgeom(Lx, Ly, H);
+    int64_t plane = g.NX * g.NY;
+    double *a = calloc((size_t)Q * plane, sizeof(double));
+    double *b = calloc((size_t)Q * plane, sizeof(double));
+    if (!a || !b) { free(a); free(b); return 5; }
+    for (int l = 0; l < Q; ++l)
+        for (int64_t x = 0; x < Lx; ++x)
+            memcpy(a + l * plane + (x + H) * g.NY + H, f_in + (l * Lx + x) * Ly,
+                   sizeof(double) * Ly);
+    int e = 0;
+    for (int64_t s = 0; s < warmup && !e; ++s) {
+        e = orc_step(a, b, Lx, Ly, H, ymode, params6, order, NULL);
+        double *t = a; a = b; b = t;
+    }
+    struct timespec t0, t1;
+    clock_gettime(CLOCK_MONOTONIC, &t0);
+    for (int64_t s = 0; s < steps && !e; ++s) {
+        e = orc_step(a, b, Lx, Ly, H, ymode, params6, order, NULL);
+        double *t = a; a = b; b = t;
+    }
+    clock_gettime(CLOCK_MONOTONIC, &t1);
+    *seconds = (double)(t1.tv_sec - t0.tv_sec) + 1e-9 * (double)(t1.tv_nsec - t0.tv_nsec);
     for (int l = 0; l < Q; ++l)
         for (int64_t x = 0; x < Lx; ++x)
             memcpy(f_out + (l * Lx + x) * Ly, a + l * plane + (x + H) * g.NY + H,

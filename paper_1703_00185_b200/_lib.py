@@ -79,6 +79,7 @@ SIGNATURES = [
     ("tlb_collide", _INT, [_FP, _FP, TlbRegion, _PP, _INT, _P, _P]),
     ("tlb_fused", _INT, [_FP, _FP, TlbRegion, _PP, _INT, _P, _P]),
     ("tlb_step_self", _INT, [_FP, _FP, _PP, _INT, _INT, _INT, _P, _P]),
+    ("tlb_step2_self", _INT, [_FP, _FP, _PP, _INT, _INT, _INT, _P, _P, _INT, _P]),
     ("tlb_moments", _INT, [_FP, TlbRegion, _P, _P, _P, _P, _I64, _INT, _P, _P]),
     ("tlb_equilibrium", _INT, [_P, _P, _P, _P, _I64, _INT, _INT, _P, _I64, _INT, _P, _P]),
     ("tlb_apply_shift", _INT, [_P, _P, _P, _I64, _PP, _P, _P, _P, _P, _P]),

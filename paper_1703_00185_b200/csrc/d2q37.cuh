@@ -83,8 +83,9 @@ struct Phys {
     int order;
 };
 
-// Defined here: the library is a single translation unit (no -rdc).
-__constant__ StencilConst C;
+// One copy per translation unit (internal linkage, no -rdc): tlb_set_stencil
+// uploads the same table into each (tlb.cu, tb2.cu).
+static __constant__ StencilConst C;
 
 // Population accessors: the arithmetic below reads f_l through get(l) and
 // writes results through put(l, v), so the same code runs on a
@@ -462,19 +463,52 @@ __device__ __forceinline__ void fast_all(F &f, const FastSite &e, double omr) {
 template <int ORDER, class F>
 __device__ __forceinline__ unsigned collide_fast(F &f, const Phys &P);
 
+// Fast moments over +/-c pairs: with s = f_c + f_-c and d = f_c - f_-c,
+// rho = f_0 + sum s, m = sum c d, e2 = sum_shell |c|^2 (sum of the shell's
+// s) -- a third of the FMAs of the direct sums, and every shell an
+// independent partial sum (short dependency chains: the two-step kernel
+// runs only 2 warps per scheduler).
+template <int sh, class FM>
+__device__ __forceinline__ void fast_shell_moments(const FM &fm, double &S, double &mx,
+                                                   double &my) {
+    constexpr int s0 = SH_START(sh), n = SH_N(sh);
+    S = 0.0;
+    mx = 0.0;
+    my = 0.0;
+#pragma unroll
+    for (int i = 0; i < n / 2; ++i) {
+        const int l = s0 + i, lm = s0 + n - 1 - i;
+        const double a = fm.get(l), b = fm.get(lm);
+        const double sp = a + b, dm = a - b;
+        S += sp;
+        if (CX(l)) mx = fma((double)CX(l), dm, mx);
+        if (CY(l)) my = fma((double)CY(l), dm, my);
+    }
+}
+
+template <class FM>
+__device__ __forceinline__ void fast_moments(const FM &fm, double &rho, double &mx, double &my,
+                                             double &e2) {
+    double S1, S2, S3, S4, S5, S6, S7, x1, x2, x3, x4, x5, x6, x7, y1, y2, y3, y4, y5, y6, y7;
+    fast_shell_moments<1>(fm, S1, x1, y1);
+    fast_shell_moments<2>(fm, S2, x2, y2);
+    fast_shell_moments<3>(fm, S3, x3, y3);
+    fast_shell_moments<4>(fm, S4, x4, y4);
+    fast_shell_moments<5>(fm, S5, x5, y5);
+    fast_shell_moments<6>(fm, S6, x6, y6);
+    fast_shell_moments<7>(fm, S7, x7, y7);
+    rho = ((fm.get(0) + S1) + (S2 + S3)) + ((S4 + S5) + (S6 + S7));
+    mx = ((x1 + x2) + (x3 + x4)) + ((x5 + x6) + x7);
+    my = ((y1 + y2) + (y3 + y4)) + ((y5 + y6) + y7);
+    // |c|^2 per shell: 1, 2, 4, 5, 8, 9, 10
+    e2 = fma(10.0, S7, fma(9.0, S6, fma(8.0, S5, 5.0 * S4))) +
+         fma(4.0, S3, fma(2.0, S2, S1));
+}
+
 template <int ORDER, class FM, class F>
 __device__ __forceinline__ unsigned collide_fast2(const FM &fm, F &f, const Phys &P) {
-    double r0 = 0.0, r1 = 0.0, mx = 0.0, my = 0.0, e2 = 0.0;
-#pragma unroll
-    for (int l = 0; l < Q; ++l) {
-        const double fl = fm.get(l);
-        if (l & 1) r1 += fl; else r0 += fl;
-        if (CX(l)) mx = fma((double)CX(l), fl, mx);
-        if (CY(l)) my = fma((double)CY(l), fl, my);
-        if (CX(l) * CX(l) + CY(l) * CY(l))
-            e2 = fma((double)(CX(l) * CX(l) + CY(l) * CY(l)), fl, e2);
-    }
-    const double rho = r0 + r1;
+    double rho, mx, my, e2;
+    fast_moments(fm, rho, mx, my, e2);
     if (!(rho > 0.0)) return 1u;
     const double ri = 1.0 / rho;
     const double ux = mx * ri, uy = my * ri;

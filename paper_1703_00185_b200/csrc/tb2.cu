@@ -1,0 +1,469 @@
+// tb2.cu -- two time steps per launch (temporal blocking) for a tile that is
+// its own X neighbour (one rank: Np = 1, the BASELINE configs[1] step).
+//
+// The single-step fused kernel moves the algorithmic minimum of ONE step
+// (592 B/site) at the HBM roofline; the only way past it is to stop writing
+// the intermediate state to HBM.  Here each CTA owns a strip of at most
+// HS = 122 output rows and marches along X over a run of columns:
+//
+//   level 1 (step s):   a column of ROWS = HS + 6 sites (the strip plus 3
+//                       rows of halo each side) is gathered from the level-0
+//                       field in HBM (implicit periodic-X / wall-clamped or
+//                       periodic-Y halos, exactly as the fused kernel),
+//                       bc + collide in registers, and stored into a
+//                       shared-memory ring;
+//   level 2 (step s+1): the column 3 behind is gathered from the ring (the
+//                       pull of propagate, kernels.py:168-177, served from
+//                       shared memory), bc + collide, and streamed to HBM.
+//
+// Level-1 rows outside the lattice are materialised in the ring as the
+// reference's halos of the intermediate state would be: wall ranks' halo rows
+// are the extension of the first/last physical row (_extend_wall_halos,
+// runtime.py:296-305: the thread computes that physical site), periodic Y
+// wraps.  Per site update that is 296 B read + 296 B written per TWO steps
+// (plus ~5 % strip/run overlap), against 592 B per step.
+//
+// The ring keeps population l of a level-1 column only as long as level 2
+// needs it: column X is read by level-2 column X + c_x, so the ring of the
+// populations with c_x = c is LANES + 3 + c columns deep (185 column slots
+// for LANES = 2: 185 KB at 128 rows, one CTA of 8 warps per SM).  Columns
+// are processed LANES at a time; the level-0 gather of the next columns is
+// issued before the level-2 half so its HBM latency hides behind it.  Work
+// items are runs of columns of one strip, handed out dynamically (an atomic
+// counter); each run starts with a 3-column warm-up.
+//
+// Parity: the same per-site arithmetic as the fused kernel (d2q37.cuh), so
+// two steps here are bitwise two fused steps (exact) -- tests compare with
+// the C oracle.  Negatives (count_negative, kernels.py:227-229) are counted
+// per step for the owned sites only; per-site failures are reported with
+// their step.
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "d2q37.cuh"
+#include "tb2.cuh"
+
+namespace tlb {
+namespace tb2 {
+
+// populations with c_x = c (c = -3..3), their ring depth and base slot
+__host__ __device__ constexpr int GN(int c) {
+    constexpr int t[7] = {3, 5, 7, 7, 7, 5, 3};
+    return t[c + 3];
+}
+template <int LANES>
+__host__ __device__ constexpr int GD(int c) { return LANES + 3 + c; }
+template <int LANES>
+__host__ __device__ constexpr int GBASE(int c) {
+    int b = 0;
+    for (int k = -3; k < c; ++k) b += GN(k) * GD<LANES>(k);
+    return b;
+}
+__host__ __device__ constexpr int GIDX(int l) {
+    int i = 0;
+    for (int m = 0; m < l; ++m) i += CX(m) == CX(l);
+    return i;
+}
+static_assert(GBASE<2>(4) == slots(2), "ring slots");
+
+// slot (in units of ROWS doubles) of population l in ring column slot s
+template <int LANES, int l>
+__device__ __forceinline__ int slot_of(const int (&s)[7]) {
+    return GBASE<LANES>(CX(l)) + s[CX(l) + 3] * GN(CX(l)) + GIDX(l);
+}
+
+// level-1 outputs go straight into the ring as they are produced
+template <int ROWS, int LANES>
+struct RingPut {
+    double (&a)[Q];
+    double *row;           // ring + this thread's row
+    const int (&ws)[7];    // write slot per c_x group
+    unsigned neg;
+    __device__ __forceinline__ double get(int l) const { return a[l]; }
+    __device__ __forceinline__ void put(int l, double v) {
+        switch (l) {
+#define TLB_RP(L) case L: row[slot_of<LANES, L>(ws) * ROWS] = v; break;
+            TLB_RP(0) TLB_RP(1) TLB_RP(2) TLB_RP(3) TLB_RP(4) TLB_RP(5) TLB_RP(6) TLB_RP(7)
+            TLB_RP(8) TLB_RP(9) TLB_RP(10) TLB_RP(11) TLB_RP(12) TLB_RP(13) TLB_RP(14)
+            TLB_RP(15) TLB_RP(16) TLB_RP(17) TLB_RP(18) TLB_RP(19) TLB_RP(20) TLB_RP(21)
+            TLB_RP(22) TLB_RP(23) TLB_RP(24) TLB_RP(25) TLB_RP(26) TLB_RP(27) TLB_RP(28)
+            TLB_RP(29) TLB_RP(30) TLB_RP(31) TLB_RP(32) TLB_RP(33) TLB_RP(34) TLB_RP(35)
+            TLB_RP(36)
+#undef TLB_RP
+        }
+        neg += (unsigned)(v < 0.0);
+    }
+};
+
+// level-2 outputs stream to HBM
+struct GlobalPut {
+    double (&a)[Q];
+    char *dp;
+    const long long *doffb;
+    unsigned neg;
+    __device__ __forceinline__ double get(int l) const { return a[l]; }
+    __device__ __forceinline__ void put(int l, double v) {
+        *reinterpret_cast<double *>(dp + doffb[l]) = v;
+        neg += (unsigned)(v < 0.0);
+    }
+};
+
+template <int ROWS, int LANES, int l>
+__device__ __forceinline__ void ring_get(double (&g)[Q], const double *row, const int (&rs)[7]) {
+    g[l] = row[slot_of<LANES, l>(rs) * ROWS - CY(l)];
+}
+template <int ROWS, int LANES, int... Ls>
+struct RingGet {
+    __device__ __forceinline__ static void run(double (&g)[Q], const double *row,
+                                               const int (&rs)[7]) {
+        (ring_get<ROWS, LANES, Ls>(g, row, rs), ...);
+    }
+};
+
+// level-0 gather for the level-1 site (x, y) (physical coordinates)
+__device__ __forceinline__ void gather0(double (&f)[Q], const TbLaunch &T, int x, int y) {
+    const Fld &S = T.src;
+    const bool inner = x >= S.Hx + 3 && x < S.Hx + S.Lx - 3 && y >= S.Hy + 3 &&
+                       y < S.Hy + S.Ly - 3;
+    if (inner) {
+        const char *sp = reinterpret_cast<const char *>(S.base + (long long)x * S.sx +
+                                                        (long long)y * S.sy);
+#pragma unroll
+        for (int l = 0; l < Q; ++l) f[l] = __ldg(reinterpret_cast<const double *>(sp + T.soffb[l]));
+    } else {
+        load_all<false>(f, S, x, y, true, true, T.flags);
+    }
+}
+
+template <bool EXACT>
+__device__ __forceinline__ unsigned walls(double (&f)[Q], const TbLaunch &T, int y) {
+    unsigned bits = 0;
+    const bool bot = y >= T.bot_lo && y < T.bot_hi;
+    const bool top = y >= T.top_lo && y < T.top_hi;
+    if (bot || top) {
+        // bottom wall then top wall, like bc() (kernels.py:190-203)
+#pragma unroll 1
+        for (int side = 0; side < 2; ++side) {
+            if (!(side ? top : bot)) continue;
+            const double Tw = side ? T.P.Ttop : T.P.Tbot;
+            RegF rf{f};
+            bits |= EXACT ? bc_exact<4>(rf, Tw) : bc_fast<4>(rf, Tw);
+        }
+    }
+    return bits;
+}
+
+// Work item i -> (strip, first column, end column), padded coordinates.
+// Wall strips (bc rows: slower per column) come first, in runs of half
+// length, so the dynamic schedule ends on short uniform runs.
+__device__ __forceinline__ void item_of(const TbLaunch &T, long long i, int &strip, int &xa,
+                                        int &xb) {
+    const int Lx = T.src.Lx;
+    const long long nh = (long long)T.nheavy * T.hruns;
+    if (i < nh) {
+        const int h = (int)(i / T.hruns);
+        strip = h == 0 ? 0 : T.ns - 1;
+        const int r = (int)(i % T.hruns);
+        xa = r * T.run_h;
+        xb = xa + T.run_h < Lx ? xa + T.run_h : Lx;
+    } else {
+        i -= nh;
+        strip = T.first_light + (int)(i / T.lruns);
+        const int r = (int)(i % T.lruns);
+        xa = r * T.run_l;
+        xb = xa + T.run_l < Lx ? xa + T.run_l : Lx;
+    }
+    xa += T.src.Hx;
+    xb += T.src.Hx;
+}
+
+template <bool EXACT, int ROWS, int LANES, int MINB>
+__global__ void __launch_bounds__(ROWS * LANES, MINB) k_tb2(const __grid_constant__ TbLaunch T) {
+    extern __shared__ double ring[];
+    __shared__ long long s_item;
+    const int lane = threadIdx.x / ROWS, r = threadIdx.x % ROWS;
+    const Fld &S = T.src;
+    const int Lx = S.Lx, Ly = S.Ly, Hx = S.Hx, Hy = S.Hy;
+    double *row = ring + r;
+    unsigned neg1 = 0, neg2 = 0;
+    for (;;) {
+        // dynamic schedule: the next work item (one strip run) for the CTA
+        if (threadIdx.x == 0) s_item = (long long)atomicAdd(T.ctr, 1u);
+        __syncthreads();
+        const long long item = s_item;
+        if (item >= T.items) break;
+        int strip, xa, xb;
+        item_of(T, item, strip, xa, xb);
+        const int ys = Hy + (int)((long long)Ly * strip / T.ns);
+        const int hs = Hy + (int)((long long)Ly * (strip + 1) / T.ns) - ys;
+        // this thread's level-1 row and the physical site it stands for
+        const int y1 = ys - 3 + r;
+        const bool row1 = r < hs + 6;
+        int y1s = y1;
+        if (T.flags & TLB_F_WRAP_Y) {
+            if (y1s < Hy) y1s += Ly;
+            else if (y1s >= Hy + Ly) y1s -= Ly;
+        } else {
+            y1s = y1s < Hy ? Hy : (y1s >= Hy + Ly ? Hy + Ly - 1 : y1s);
+        }
+        const bool row2 = r >= 3 && r < hs + 3;   // level-2 row y1 is an output row
+        const int K = (xb - xa + 6 + LANES - 1) / LANES;
+        auto wrapx = [&](int x) { return x < Hx ? x + Lx : (x >= Hx + Lx ? x - Lx : x); };
+        double f[Q];
+        if (row1) gather0(f, T, wrapx(xa - 3 + lane), y1s);
+        // ring slots of level-1 column j (written) and of the columns level 2
+        // reads (j - 3 - c), per c_x group; advanced by LANES per iteration
+        int ws[7], rs[7];
+#pragma unroll
+        for (int c = -3; c <= 3; ++c) {
+            ws[c + 3] = lane % GD<LANES>(c);
+            rs[c + 3] = (lane + 2 * GD<LANES>(c) - 3 - c) % GD<LANES>(c);
+        }
+        for (int k = 0; k < K; ++k) {
+            const int j = LANES * k + lane;      // ring column of this level-1 column
+            const int X1 = xa - 3 + j;           // level-1 column (unwrapped)
+            if (row1 && X1 < xb + 3) {
+                const int xs = wrapx(X1);
+                unsigned bits = walls<EXACT>(f, T, y1s);
+                RingPut<ROWS, LANES> rp{f, row, ws, 0u};
+                bits |= EXACT ? collide_exact<4>(rp, T.P) : collide_fast<4>(rp, T.P);
+                if (bits) report(T.st1, bits, xs, y1s, T.step);
+                if (row2 && X1 >= xa && X1 < xb) neg1 += rp.neg;
+            }
+            // the next level-1 column's HBM gather, in flight during level 2
+            if (row1 && k + 1 < K && X1 + LANES < xb + 3) gather0(f, T, wrapx(X1 + LANES), y1s);
+            __syncthreads();
+            const int X2 = X1 - 3;
+            if (row2 && X2 >= xa && X2 < xb) {
+                double g[Q];
+                RingGet<ROWS, LANES, 0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16, 17,
+                        18, 19, 20, 21, 22, 23, 24, 25, 26, 27, 28, 29, 30, 31, 32, 33, 34, 35,
+                        36>::run(g, row, rs);
+                unsigned bits = walls<EXACT>(g, T, y1);
+                char *dp = reinterpret_cast<char *>(T.dst.base + (long long)X2 * T.dst.sx +
+                                                    (long long)y1 * T.dst.sy);
+                GlobalPut gp{g, dp, T.doffb, 0u};
+                bits |= EXACT ? collide_exact<4>(gp, T.P) : collide_fast<4>(gp, T.P);
+                if (bits) report(T.st2, bits, X2, y1, T.step + 1);
+                neg2 += gp.neg;
+            }
+#pragma unroll
+            for (int c = -3; c <= 3; ++c) {
+                ws[c + 3] += LANES;
+                if (ws[c + 3] >= GD<LANES>(c)) ws[c + 3] -= GD<LANES>(c);
+                rs[c + 3] += LANES;
+                if (rs[c + 3] >= GD<LANES>(c)) rs[c + 3] -= GD<LANES>(c);
+            }
+            __syncthreads();
+        }
+    }
+    if (T.flags & TLB_F_COUNT_NEG) {
+        count_neg_n(T.st1, neg1);
+        count_neg_n(T.st2, neg2);
+    }
+}
+
+template <bool EXACT, int ROWS, int LANES, int MINB>
+static cudaError_t launch_cfg(const TbLaunch &T, int sms, cudaStream_t s) {
+    const size_t smem = (size_t)slots(LANES) * ROWS * sizeof(double);
+    static bool attr = false;
+    auto *fn = k_tb2<EXACT, ROWS, LANES, MINB>;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    long long grid = (long long)sms * MINB;
+    if (grid > T.items) grid = T.items;
+    fn<<<(unsigned)grid, ROWS * LANES, smem, s>>>(T);
+    return cudaGetLastError();
+}
+
+
+// ------------------------------------------------ warp-specialised variant --
+// Producer warps (level 1: HBM gather, bc + collide, ring) and consumer warps
+// (level 2: ring gather, bc + collide, HBM) run concurrently.  They meet only
+// at shared-memory mbarriers: full[column] (all ROWS producer threads of a
+// level-1 column arrived) and empty[column] (all consumer threads of a
+// level-2 column arrived), so no warp waits at a CTA-wide barrier inside a
+// run.  The ring slack is E - 3 columns: the producer of level-1 column j
+// may overwrite its slots once level-2 column j - E - 3 is done.
+__device__ __forceinline__ void mb_init(unsigned long long *b, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(
+                     (unsigned)__cvta_generic_to_shared(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mb_arrive(unsigned long long *b) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(
+                     (unsigned)__cvta_generic_to_shared(b)) : "memory");
+}
+__device__ __forceinline__ void mb_wait(unsigned long long *b, unsigned parity) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(b);
+    unsigned done = 0;
+    do {
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;"
+                     " selp.u32 %0, 1, 0, p; }" : "=r"(done) : "r"(a), "r"(parity) : "memory");
+    } while (!done);
+}
+
+constexpr int NBAR = 32;   // full / empty barriers (column index mod NBAR)
+
+template <bool EXACT, int ROWS, int PL, int CL, int E, int MINB>
+__global__ void __launch_bounds__(ROWS * (PL + CL), MINB) k_tb2ws(const __grid_constant__ TbLaunch T) {
+    constexpr int LANES = E - 3;        // ring depth of group c: E + c = GD<LANES>(c)
+    constexpr int WPC = ROWS / 32;      // warps per column
+    extern __shared__ double ring[];
+    __shared__ unsigned long long full[NBAR], empty[NBAR];
+    __shared__ long long s_item;
+    const int warp = threadIdx.x / 32;
+    const bool producer = warp < PL * WPC;
+    const int lane = producer ? warp / WPC : (warp - PL * WPC) / WPC;
+    const int r = (warp % WPC) * 32 + (threadIdx.x & 31);
+    const Fld &S = T.src;
+    const int Lx = S.Lx, Ly = S.Ly, Hx = S.Hx, Hy = S.Hy;
+    double *row = ring + r;
+    unsigned neg1 = 0, neg2 = 0;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NBAR; ++i) {
+            mb_init(&full[i], ROWS);               // every thread of the producing column
+            mb_init(&empty[i], ROWS);              // every thread of the consuming column
+        }
+    }
+    long long gj = 0, gm = 0;   // level-1 / level-2 columns of earlier runs (barrier phases)
+    for (;;) {
+        if (threadIdx.x == 0) s_item = (long long)atomicAdd(T.ctr, 1u);
+        __syncthreads();        // also: the previous run has drained
+        const long long item = s_item;
+        __syncthreads();
+        if (item >= T.items) break;
+        int strip, xa, xb;
+        item_of(T, item, strip, xa, xb);
+        const int ys = Hy + (int)((long long)Ly * strip / T.ns);
+        const int hs = Hy + (int)((long long)Ly * (strip + 1) / T.ns) - ys;
+        const int y1 = ys - 3 + r;
+        const int w = xb - xa, NJ = w + 6;
+        auto wrapx = [&](int x) { return x < Hx ? x + Lx : (x >= Hx + Lx ? x - Lx : x); };
+        if (producer) {
+            const bool row1 = r < hs + 6;
+            int y1s = y1;
+            if (T.flags & TLB_F_WRAP_Y) {
+                if (y1s < Hy) y1s += Ly;
+                else if (y1s >= Hy + Ly) y1s -= Ly;
+            } else {
+                y1s = y1s < Hy ? Hy : (y1s >= Hy + Ly ? Hy + Ly - 1 : y1s);
+            }
+            const bool own_row = r >= 3 && r < hs + 3;
+            for (int j = lane; j < NJ; j += PL) {
+                const int X1 = xa - 3 + j;
+                double f[Q];
+                if (row1) gather0(f, T, wrapx(X1), y1s);
+                if (j >= E + 3) {
+                    const long long m = gm + (j - E - 3);
+                    mb_wait(&empty[m % NBAR], (unsigned)((m / NBAR) & 1));
+                }
+                if (row1) {
+                    int wsl[7];
+#pragma unroll
+                    for (int c = -3; c <= 3; ++c) wsl[c + 3] = j % GD<LANES>(c);
+                    unsigned bits = walls<EXACT>(f, T, y1s);
+                    RingPut<ROWS, LANES> rp{f, row, wsl, 0u};
+                    bits |= EXACT ? collide_exact<4>(rp, T.P) : collide_fast<4>(rp, T.P);
+                    if (bits) report(T.st1, bits, wrapx(X1), y1s, T.step);
+                    if (own_row && X1 >= xa && X1 < xb) neg1 += rp.neg;
+                }
+                const long long g = gj + j;
+                mb_arrive(&full[g % NBAR]);
+            }
+        } else {
+            const bool row2 = r >= 3 && r < hs + 3;
+            for (int m = lane; m < w; m += CL) {
+                for (int j = m; j <= m + 6; ++j) {
+                    const long long g = gj + j;
+                    mb_wait(&full[g % NBAR], (unsigned)((g / NBAR) & 1));
+                }
+                if (row2) {
+                    int rsl[7];
+#pragma unroll
+                    for (int c = -3; c <= 3; ++c) rsl[c + 3] = (m + 3 - c) % GD<LANES>(c);
+                    double g2[Q];
+                    RingGet<ROWS, LANES, 0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16,
+                            17, 18, 19, 20, 21, 22, 23, 24, 25, 26, 27, 28, 29, 30, 31, 32, 33, 34,
+                            35, 36>::run(g2, row, rsl);
+                    const int X2 = xa + m;
+                    unsigned bits = walls<EXACT>(g2, T, y1);
+                    char *dp = reinterpret_cast<char *>(T.dst.base + (long long)X2 * T.dst.sx +
+                                                        (long long)y1 * T.dst.sy);
+                    GlobalPut gp{g2, dp, T.doffb, 0u};
+                    bits |= EXACT ? collide_exact<4>(gp, T.P) : collide_fast<4>(gp, T.P);
+                    if (bits) report(T.st2, bits, X2, y1, T.step + 1);
+                    neg2 += gp.neg;
+                }
+                const long long g = gm + m;
+                mb_arrive(&empty[g % NBAR]);
+            }
+        }
+        gj += NJ;
+        gm += w;
+    }
+    if (T.flags & TLB_F_COUNT_NEG) {
+        count_neg_n(T.st1, neg1);
+        count_neg_n(T.st2, neg2);
+    }
+}
+
+template <bool EXACT, int ROWS, int PL, int CL, int E, int MINB>
+static cudaError_t launch_ws(const TbLaunch &T, int sms, cudaStream_t s) {
+    const size_t smem = (size_t)37 * E * ROWS * sizeof(double);
+    static bool attr = false;
+    auto *fn = k_tb2ws<EXACT, ROWS, PL, CL, E, MINB>;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    long long grid = (long long)sms * MINB;
+    if (grid > T.items) grid = T.items;
+    fn<<<(unsigned)grid, ROWS * (PL + CL), smem, s>>>(T);
+    return cudaGetLastError();
+}
+
+}  // namespace tb2
+
+cudaError_t tb2_set_const(const StencilConst &h) {
+    return cudaMemcpyToSymbol(C, &h, sizeof h);
+}
+
+int tb2_rows(int cfg) {
+    return (cfg == 1 || cfg == 4) ? 64 : (cfg == 2 || cfg == 6) ? 96 : 128;
+}
+
+cudaError_t tb2_launch(const tb2::TbLaunch &T, bool exact, int cfg, int sms, cudaStream_t s) {
+    // cfg 0: 128 rows x 2 lanes, 1 CTA/SM; 1: 64 x 2, 2 CTAs/SM; 2: 96 x 2, 1 CTA/SM
+    switch (cfg) {
+    case 1:
+        return exact ? tb2::launch_cfg<true, 64, 2, 2>(T, sms, s)
+                     : tb2::launch_cfg<false, 64, 2, 2>(T, sms, s);
+    case 2:
+        return exact ? tb2::launch_cfg<true, 96, 2, 1>(T, sms, s)
+                     : tb2::launch_cfg<false, 96, 2, 1>(T, sms, s);
+    // warp-specialised: rows, producer lanes, consumer lanes, ring depth E, CTAs/SM
+    case 3:
+        return exact ? tb2::launch_ws<true, 128, 2, 2, 6, 1>(T, sms, s)
+                     : tb2::launch_ws<false, 128, 2, 2, 6, 1>(T, sms, s);
+    case 4:
+        return exact ? tb2::launch_ws<true, 64, 2, 2, 5, 2>(T, sms, s)
+                     : tb2::launch_ws<false, 64, 2, 2, 5, 2>(T, sms, s);
+    case 5:
+        return exact ? tb2::launch_ws<true, 128, 3, 1, 6, 1>(T, sms, s)
+                     : tb2::launch_ws<false, 128, 3, 1, 6, 1>(T, sms, s);
+    case 6:
+        return exact ? tb2::launch_ws<true, 96, 2, 2, 8, 1>(T, sms, s)
+                     : tb2::launch_ws<false, 96, 2, 2, 8, 1>(T, sms, s);
+    default:
+        return exact ? tb2::launch_cfg<true, 128, 2, 1>(T, sms, s)
+                     : tb2::launch_cfg<false, 128, 2, 1>(T, sms, s);
+    }
+}
+
+}  // namespace tlb

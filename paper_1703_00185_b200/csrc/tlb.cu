@@ -16,7 +16,9 @@
 #include <string>
 
 #include "../../include/tlb.h"
+#include "common.cuh"
 #include "d2q37.cuh"
+#include "tb2.cuh"
 
 using namespace tlb;
 
@@ -49,35 +51,12 @@ static int launch_check(const char *what) {
 
 static bool g_stencil_set[64];
 static int g_minb = 4;    // tuning: __launch_bounds__ min blocks of the fused kernel
-
-// --------------------------------------------------------- device helpers --
-struct Fld {
-    double *base;
-    long long sl, sx, sy;
-    int Lx, Ly, Hx, Hy;
-};
-
-static Fld mkfld(const TlbField *f) {
-    Fld d;
-    d.base = f->base;
-    d.sl = f->sl; d.sx = f->sx; d.sy = f->sy;
-    d.Lx = f->Lx; d.Ly = f->Ly; d.Hx = f->Hx; d.Hy = f->Hy;
-    return d;
-}
-
-static Phys mkphys(const TlbParams *p) {
-    // exactly the reference's host-side expressions (kernels.py:130-133, 145)
-    Phys P;
-    P.K1 = p->tau * p->gx;
-    P.K2 = p->tau * p->gy;
-    double g2 = p->gx * p->gx + p->gy * p->gy;
-    P.K3 = p->tau * p->tau * g2 / 2.0;
-    P.omega = p->dt / p->tau;
-    P.Tbot = p->Twall_bot;
-    P.Ttop = p->Twall_top;
-    P.order = p->order;
-    return P;
-}
+// two-step kernel (tb2.cu) shape and work-item length: 64-row strips, 2
+// columns per iteration, 2 CTAs per SM, runs of 128 columns -- measured
+// best on B200 (tools/tb2_probe.py, profiles/r02_tb2.md)
+static int g_tb2_cfg = 1;
+static int g_tb2_run = 128;
+static unsigned *g_tb2_ctr[64];  // two-step work-item counters (one u32 per device)
 
 // A launch covers an interior rectangle (plain gather: no halo remapping,
 // no wall rows -- the hot path) plus up to four frame rectangles (implicit
@@ -103,102 +82,7 @@ struct SiteLaunch {
     int step;
 };
 
-__device__ __forceinline__ void report(TlbStatus *st, unsigned bits, int x, int y, int step) {
-    if (!bits || !st) return;
-    unsigned old = atomicOr(&st->flags, bits);
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        if ((bits >> k & 1u) && !(old >> k & 1u)) {
-            st->site_x[k] = x;
-            st->site_y[k] = y;
-            st->step = step;
-        }
-    }
-}
-
-// Block-level count of negative populations: one atomic per CTA that saw
-// any (count_negative, monitoring only).
-__device__ __forceinline__ void count_neg_n(TlbStatus *st, unsigned n) {
-    n = __reduce_add_sync(0xffffffffu, n);
-    if (__syncthreads_or(n != 0)) {
-        __shared__ unsigned warp_n[32];
-        if ((threadIdx.x & 31) == 0) warp_n[threadIdx.x >> 5] = n;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            unsigned t = 0;
-            for (unsigned w = 0; w < (blockDim.x + 31) / 32; ++w) t += warp_n[w];
-            if (t) atomicAdd(&st->negatives, (unsigned long long)t);
-        }
-    }
-}
-
-__device__ __forceinline__ void count_neg(TlbStatus *st, const double (&f)[Q], bool active) {
-    unsigned n = 0;
-    if (active) {
-#pragma unroll
-        for (int l = 0; l < Q; ++l) n += f[l] < 0.0;
-    }
-    count_neg_n(st, n);
-}
-
 enum Kind { K_PROPAGATE = 0, K_BC = 1, K_COLLIDE = 2, K_FUSED = 3 };
-
-// Source coordinate of population l's pull for site (x, y) with implicit
-// halos (TLB_F_WRAP_X / WRAP_Y / CLAMP_Y), else the halo memory itself.
-__device__ __forceinline__ int src_x(int x, int cx, const Fld &s, int flags) {
-    int xs = x - cx;
-    if (flags & TLB_F_WRAP_X) {
-        if (xs < s.Hx) xs += s.Lx;
-        else if (xs >= s.Hx + s.Lx) xs -= s.Lx;
-    }
-    return xs;
-}
-__device__ __forceinline__ int src_y(int y, int cy, const Fld &s, int flags) {
-    int ys = y - cy;
-    if (flags & TLB_F_WRAP_Y) {
-        if (ys < s.Hy) ys += s.Ly;
-        else if (ys >= s.Hy + s.Ly) ys -= s.Ly;
-    } else {
-        if ((flags & TLB_F_CLAMP_BOT) && ys < s.Hy) ys = s.Hy;
-        if ((flags & TLB_F_CLAMP_TOP) && ys >= s.Hy + s.Ly) ys = s.Hy + s.Ly - 1;
-    }
-    return ys;
-}
-
-// COH: coherent L2 loads (ld.global.cg) for data other GPUs write while the
-// kernel runs (the peer step's halos); else the read-only path (__ldg).
-template <int l, bool COH = false>
-__device__ __forceinline__ void load_one(double (&f)[Q], const Fld &s, int x, int y,
-                                         bool gather, bool implicit, int flags) {
-    int xs = x, ys = y;
-    if (gather) {
-        if (implicit) {
-            xs = src_x(x, CX(l), s, flags);
-            ys = src_y(y, CY(l), s, flags);
-        } else {
-            xs = x - CX(l);
-            ys = y - CY(l);
-        }
-    }
-    const double *p = s.base + (long long)l * s.sl + (long long)xs * s.sx + (long long)ys * s.sy;
-    f[l] = COH ? __ldcg(p) : __ldg(p);
-}
-
-template <bool COH, int... Ls>
-struct LoadSeq {
-    __device__ __forceinline__ static void run(double (&f)[Q], const Fld &s, int x, int y,
-                                               bool gather, bool implicit, int flags) {
-        (load_one<Ls, COH>(f, s, x, y, gather, implicit, flags), ...);
-    }
-};
-
-template <bool COH = false>
-__device__ __forceinline__ void load_all(double (&f)[Q], const Fld &s, int x, int y,
-                                         bool gather, bool implicit, int flags) {
-    LoadSeq<COH, 0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16, 17, 18, 19, 20, 21,
-            22, 23, 24, 25, 26, 27, 28, 29, 30, 31, 32, 33, 34, 35,
-            36>::run(f, s, x, y, gather, implicit, flags);
-}
 
 __device__ __forceinline__ void store_all(const double (&f)[Q], const Fld &d, int x, int y) {
     double *p = d.base + (long long)x * d.sx + (long long)y * d.sy;
@@ -698,6 +582,16 @@ extern "C" {
 int tlb_version(void) { return 1; }
 
 int tlb_set_tuning(int key, int value) {
+    if (key == TLB_TUNE_TB2_CFG) {
+        if (value < 0 || value > 6) return fail(TLB_ERR_CONTRACT, "two-step config must be 0-6");
+        g_tb2_cfg = value;
+        return TLB_OK;
+    }
+    if (key == TLB_TUNE_TB2_RUN) {
+        if (value < 8) return fail(TLB_ERR_CONTRACT, "two-step run must be >= 8 columns");
+        g_tb2_run = value;
+        return TLB_OK;
+    }
     if (key == TLB_TUNE_MINBLOCKS) {
         if (value != 1 && value != 4 && value != 5)
             return fail(TLB_ERR_CONTRACT, "min blocks must be 1, 4 or 5");
@@ -800,6 +694,7 @@ int tlb_set_stencil(int device, const int64_t *c, const double *w, double cs2) {
     TLB_CUDA_CHECK(cudaSetDevice(device));
     TLB_CUDA_CHECK(cudaDeviceSynchronize());  // no kernel may still read the old table
     TLB_CUDA_CHECK(cudaMemcpyToSymbol(C, &h, sizeof h));
+    TLB_CUDA_CHECK(tb2_set_const(h));   // the two-step kernel's copy (tb2.cu)
     int e = set_generic(device, Q, c, w, cs2);
     if (e) return e;
     TLB_CUDA_CHECK(cudaDeviceSynchronize());
@@ -921,6 +816,64 @@ int tlb_step_self(const TlbField *prv, const TlbField *nxt, const TlbParams *p, 
     if (count_neg) flags |= TLB_F_COUNT_NEG;
     TlbRegion r = {prv->Hx, prv->Hx + prv->Lx, prv->Hy, prv->Hy + prv->Ly};
     return tlb_fused(prv, nxt, r, p, flags, status, stream);
+}
+
+int tlb_step2_self(const TlbField *prv, const TlbField *nxt, const TlbParams *p, int walls,
+                   int periodic_y, int count_neg, TlbStatus *status1, TlbStatus *status2,
+                   int step, tlb_stream_t stream) {
+    int e;
+    if ((e = check_stencil())) return e;
+    if ((e = check_params(p))) return e;
+    if (device_generic()) return fail(TLB_ERR_UNSUPPORTED, "two-step kernel: D2Q37 only");
+    if (p->order != 4) return fail(TLB_ERR_UNSUPPORTED, "two-step kernel: order 4 only");
+    if (prv->Lx < 8 || prv->Ly < 8)
+        return fail(TLB_ERR_UNSUPPORTED, "two-step kernel: tile smaller than 8x8");
+    if (prv->base == nxt->base) return fail(TLB_ERR_CONTRACT, "step2: prv and nxt alias");
+    if (walls && (!(p->Twall_top > 0.0) || !(p->Twall_bot > 0.0)))
+        return fail(TLB_ERR_DOMAIN, "equilibrium requires rho > 0 and T > 0");
+    tb2::TbLaunch T;
+    memset(&T, 0, sizeof T);
+    T.src = mkfld(prv);
+    T.dst = mkfld(nxt);
+    T.P = mkphys(p);
+    int flags = TLB_F_WRAP_X;
+    if (walls) flags |= TLB_F_WALL_BOT | TLB_F_WALL_TOP | TLB_F_CLAMP_Y;
+    else if (periodic_y) flags |= TLB_F_WRAP_Y;
+    if (count_neg) flags |= TLB_F_COUNT_NEG;
+    T.flags = flags;
+    SiteLaunch W;
+    memset(&W, 0, sizeof W);
+    wall_rows(W, prv, flags);
+    T.bot_lo = W.bot_lo; T.bot_hi = W.bot_hi; T.top_lo = W.top_lo; T.top_hi = W.top_hi;
+    for (int l = 0; l < Q; ++l) {
+        T.soffb[l] = 8 * ((long long)l * T.src.sl -
+                          ((long long)CX(l) * T.src.sx + (long long)CY(l) * T.src.sy));
+        T.doffb[l] = 8 * (long long)l * T.dst.sl;
+    }
+    const int hs = tb2_rows(g_tb2_cfg) - 6;     // output rows per strip, at most
+    T.ns = (prv->Ly + hs - 1) / hs;
+    // work items: runs of run_l columns of a strip; wall strips (bc rows)
+    // first, in runs of half the length
+    const int Lx = prv->Lx;
+    T.run_l = g_tb2_run < Lx ? g_tb2_run : Lx;
+    T.run_h = T.run_l / 2 > 8 ? T.run_l / 2 : T.run_l;
+    T.nheavy = walls ? (T.ns >= 2 ? 2 : 1) : 0;
+    T.first_light = walls ? 1 : 0;
+    const int nlight = T.ns - T.nheavy;
+    T.hruns = (Lx + T.run_h - 1) / T.run_h;
+    T.lruns = (Lx + T.run_l - 1) / T.run_l;
+    T.items = (long long)T.nheavy * T.hruns + (long long)nlight * T.lruns;
+    T.st1 = status1;
+    T.st2 = status2;
+    T.step = step;
+    int dev = 0, sms = 0;
+    TLB_CUDA_CHECK(cudaGetDevice(&dev));
+    TLB_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    if (!g_tb2_ctr[dev]) TLB_CUDA_CHECK(cudaMalloc(&g_tb2_ctr[dev], sizeof(unsigned)));
+    T.ctr = g_tb2_ctr[dev];
+    TLB_CUDA_CHECK(cudaMemsetAsync(T.ctr, 0, sizeof(unsigned), (cudaStream_t)stream));
+    TLB_CUDA_CHECK(tb2_launch(T, p->arith == TLB_ARITH_EXACT, g_tb2_cfg, sms, (cudaStream_t)stream));
+    return TLB_OK;
 }
 
 int tlb_moments(const TlbField *f, TlbRegion r, double *rho, double *ux, double *uy, double *T,

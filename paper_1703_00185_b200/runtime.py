@@ -349,7 +349,8 @@ class RankWorker:
 
     def __init__(self, tile, vs, params, fabric=None, schedule="staged", walls=True,
                  layout="column", halo=DEFAULT_HALO, debug_poison=False, device=None,
-                 periodic_y=False, exchange="auto", timing="sampled", timing_every=32):
+                 periodic_y=False, exchange="auto", timing="sampled", timing_every=32,
+                 temporal="auto"):
         torch = _lib.torch_cuda()
         if schedule not in ("staged", "overlapped"):
             raise ConfigurationError(f"unknown schedule {schedule!r}")
@@ -357,6 +358,9 @@ class RankWorker:
             raise ConfigurationError(f"unknown exchange {exchange!r} (auto|nccl|p2p)")
         if timing not in ("sampled", "every", "off"):
             raise ConfigurationError(f"unknown timing {timing!r} (sampled|every|off)")
+        if temporal not in ("auto", "on", "off"):
+            raise ConfigurationError(f"unknown temporal {temporal!r} (auto|on|off)")
+        self.temporal = temporal
         self.timing, self.timing_every, self._count = timing, max(1, int(timing_every)), 0
         self.tile = tile
         self.vs = vs
@@ -745,6 +749,52 @@ class RankWorker:
         return (self.x_self and not self.y_exchange and self._ring is None
                 and self._peer is None and not self.debug_poison and self.timing != "every")
 
+    def pairable(self):
+        """Two steps per launch (temporal blocking, csrc/tb2.cu): a single
+        self-periodic tile with the overlapped schedule, D2Q37 order 4, at
+        least 8x8.  "auto" takes it for the fast arithmetic (where it is the
+        faster kernel); "on" for both arithmetics; results are the same bits
+        as two single steps either way."""
+        if self.temporal == "off" or self.schedule != "overlapped" or self.debug_poison:
+            return False
+        order = self.params.eq_order if self.params.eq_order is not None else self.vs.eq_order
+        if not (self.x_self and not self.y_exchange and self._ring is None and self._peer is None
+                and (self.y_self or (self.wall_bot and self.wall_top))
+                and self.vs.Q == 37 and order == 4 and self.geom.Lx >= 8 and self.geom.Ly >= 8):
+            return False
+        return self.temporal == "on" or self.tparams.arith == _lib.ARITH["fast"]
+
+    def step_pair(self, step_no):
+        """Steps step_no and step_no + 1 in ONE launch (tlb_step2_self): the
+        intermediate state stays in shared memory.  Bitwise equal to
+        step(step_no); step(step_no + 1); per-step metrics and failures keep
+        their step numbers."""
+        torch = _lib.torch_cuda()
+        if self._capture_slot is not None:
+            s1, s2 = self._capture_slot
+        else:
+            if len(self._records) + 2 > self._RING:
+                self.collect()
+            n = len(self._records)
+            s1, s2 = self._status_ring[n], self._status_ring[n + 1]
+        timed = self.timing == "every" or (
+            self.timing == "sampled" and self._count % self.timing_every == 0)
+        self._count += 2
+        ev = None
+        if timed:
+            ev = ("graph", torch.cuda.Event(enable_timing=True),
+                  torch.cuda.Event(enable_timing=True), 2)
+            ev[1].record(self.stream)
+        self._check(_lib.load().tlb_step2_self(
+            field_desc(self.prv), field_desc(self.nxt), self.tparams, int(self.wall_bot),
+            int(self.y_self), 1, s1.data_ptr(), s2.data_ptr(), int(step_no), self._sp()),
+            "step2")
+        if ev is not None:
+            ev[2].record(self.stream)
+        self._records.append(_StepRecord(step_no, s1, ev))
+        self._records.append(_StepRecord(step_no + 1, s2, ev))
+        self.prv, self.nxt = swap_buffers(self.prv, self.nxt)
+
     def run_steps(self, step0, n):
         """Steps step0 .. step0+n-1, bitwise identical to calling step().
 
@@ -779,12 +829,18 @@ class RankWorker:
                 self._records.extend(_StepRecord(s + j, self._status_ring[pos + j], ev)
                                      for j in range(G))
                 s += G
+        pair = self.pairable()
         while s < end:
-            self.step(s)
-            s += 1
+            if pair and end - s >= 2:
+                self.step_pair(s)
+                s += 2
+            else:
+                self.step(s)
+                s += 1
 
     def _graph_for(self):
-        key = (self.prv.data.data_ptr(), self._flags(), self.schedule)
+        key = (self.prv.data.data_ptr(), self._flags(), self.schedule, self.pairable(),
+               bytes(self.tparams))
         graph = self._graphs.get(key)
         if graph is None:
             graph = self._graphs[key] = self._capture()
@@ -807,9 +863,17 @@ class RankWorker:
                 graph.capture_begin(capture_error_mode="thread_local")
                 try:
                     self._gstatus.zero_()
-                    for j in range(G):
-                        self._capture_slot = self._gstatus[j]
-                        self.step(j)
+                    pair = self.pairable()
+                    j = 0
+                    while j < G:
+                        if pair:
+                            self._capture_slot = (self._gstatus[j], self._gstatus[j + 1])
+                            self.step_pair(j)
+                            j += 2
+                        else:
+                            self._capture_slot = self._gstatus[j]
+                            self.step(j)
+                            j += 1
                 finally:
                     graph.capture_end()
         finally:
@@ -972,6 +1036,11 @@ class RankWorker:
         if not timeout:
             self.stream.synchronize()
             return
+        if self._peer is not None:
+            # the step kernel's own bounded wait (the same timeout) reports
+            # a stalled neighbour first, with its step; then later queued
+            # steps fail at once
+            timeout = 1.5 * timeout + 1.0
         ev = torch.cuda.Event()
         ev.record(self.stream)
         deadline = time.monotonic() + timeout

@@ -52,6 +52,8 @@ class SimConfig:
     exchange: str = "auto"   # one process per GPU: "p2p" (NVLink peer stores fused into the
                              # step kernel) where it applies, else the "nccl" ring
     timing: str = "sampled"  # per-step device timers: "sampled" (1 in 32), "every", "off"
+    temporal: str = "auto"   # two steps per launch on a single tile (csrc/tb2.cu): "auto"
+                             # (fast arithmetic), "on" (also exact), "off"
 
     def __post_init__(self):
         if self.schedule not in ("staged", "overlapped"):
@@ -199,7 +201,7 @@ def run(cfg: SimConfig, f0=None) -> RunResult:
                            walls=cfg.walls, layout=cfg.layout, halo=cfg.halo,
                            debug_poison=cfg.debug_poison, device=dev,
                            periodic_y=cfg.periodic_y, exchange=cfg.exchange,
-                           timing=cfg.timing)
+                           timing=cfg.timing, temporal=cfg.temporal)
         workers.append(w)
     if dist is None and cfg.Np > 1 and cfg.exchange == "p2p":
         # in-process ranks with the peer-store step kernel of one process

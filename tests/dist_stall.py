@@ -8,8 +8,8 @@ more steps: rank 0's exchange can never complete.
         NCCL ring (releasing the stalled NCCL kernels) and raises
         DeadlockError naming rank 0;
   p2p:  the step kernel's border blocks give up after their bounded wait
-        (5 s) and flag PEER_TIMEOUT; collect() raises DeadlockError naming
-        rank 0.
+        (the fabric timeout, tlb_peer_set_timeout) and flag PEER_TIMEOUT;
+        collect() raises DeadlockError naming rank 0.
 The one-process-per-GPU analog of the reference's deadlock detection
 (runtime.py:146-149, tests/test_runtime.py).  Prints "STALL OK".
 """
@@ -37,7 +37,7 @@ def main():
     p = tl.PhysicsParams(tau=0.8, gy=-1e-5, Twall_top=0.9 * vs.cs2, Twall_bot=1.1 * vs.cs2)
     tile = tl.decompose(96, 40, world, "1d")[rank]
     mode = sys.argv[1] if len(sys.argv) > 1 else "nccl"
-    fabric = tl.DistFabric(timeout=4.0 if mode == "nccl" else 30.0)
+    fabric = tl.DistFabric(timeout=4.0)
     w = tl.RankWorker(tile, vs, p, fabric, device=dev, schedule="overlapped", exchange=mode)
     assert w.exchange_mode == mode
     w.load_block(torch.full((vs.Q, tile.Lx, tile.Ly), 1.0 / vs.Q, dtype=torch.float64,
@@ -59,8 +59,8 @@ def main():
             print("rank 0: stalled step completed?!", flush=True)
         except tl.DeadlockError as exc:
             waited = time.monotonic() - t0
-            # p2p: one 5 s bounded wait, then the sticky flag fails the
-            # other queued steps at once (5 waits would take 25 s)
+            # p2p: one 4 s bounded wait, then the sticky flag fails the
+            # other queued steps at once (5 waits would take 20 s)
             ok = exc.rank == 0 and 3.5 < waited < (30.0 if mode == "nccl" else 12.0)
             print(f"rank 0 ({mode}): DeadlockError after {waited:.1f} s: {exc}", flush=True)
     flag = torch.tensor([int(ok)], device=dev)
