@@ -224,6 +224,44 @@ def cpu_oracle_rate(seconds=None, steps=None, warmup=2, Lx=TILE_LX, Ly=TILE_LY):
             f"{nthreads} threads, {el:.2f} s")
 
 
+def numpy_reference_rates(budget_s=60.0):
+    """The reference package itself (`thermolb`, pip-installed from
+    /root/reference into baseline/_ref, which travels to the GPU box) timed
+    through its public run() (sim.py:62-129; MLUPS = Lx*Ly*steps/wall,
+    :127) as SURVEY §8(d) asks: C1 RT 256x128 at Np=1 (numpy ufuncs are
+    single-threaded: one core) and C2 RT 1920x2048 at Np = the host cores
+    (1-D tiles on worker threads; numpy releases the GIL), 2 steps.
+    Returns a dict, or {"unavailable": why}."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "thermolb")):
+        return {"unavailable": "baseline/_ref not installed (see DESIGN.md)"}
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    try:
+        import thermolb
+        from thermolb import PhysicsParams, SimConfig, build_velocity_set, run
+    except Exception as e:  # noqa: BLE001 -- report, do not fail the arm
+        return {"unavailable": f"import thermolb failed: {e!r}"[:200]}
+    vs = build_velocity_set("D2Q37")
+    p = PhysicsParams(tau=0.8, gy=-1e-5, Twall_top=0.9 * vs.cs2, Twall_bot=1.1 * vs.cs2)
+    cores = len(os.sched_getaffinity(0))
+    np_c2 = max(d for d in range(1, cores + 1) if TILE_LX % d == 0)
+    out = {"package": f"thermolb {thermolb.__version__} (baseline/_ref)",
+           "api": "thermolb.run(SimConfig) (sim.py:62-129)"}
+    t_start = time.time()
+    for name, Lx, Ly, Np, steps in (("C1", 256, 128, 1, 100), ("C2", TILE_LX, TILE_LY, np_c2, 2)):
+        if time.time() - t_start > budget_s:
+            out[name] = {"skipped": f"over the {budget_s:.0f} s budget"}
+            continue
+        cfg = SimConfig(Lx=Lx, Ly=Ly, Np=Np, tiling="1d", schedule="overlapped", steps=steps,
+                        params=p, init="rayleigh-taylor")
+        res = run(cfg)
+        out[name] = {"lattice": f"{Lx}x{Ly}", "Np": Np, "cores": Np, "steps": steps,
+                     "wall_s": round(res.wall_seconds, 3), "mlups": round(res.mlups, 4),
+                     "gflops_fp64": round(res.mlups * FLOP_SITE / 1e3, 3)}
+    return out
+
+
 def reference_arm(args, rank, world):
     """--impl reference: the reference algorithm on the host CPU (the C
     oracle, every host thread) on the workload of the GPU arm's config --
@@ -258,6 +296,8 @@ def reference_arm(args, rank, world):
         "e2e": {"value": round(mlups, 4), "unit": "MLUPS", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
+    if args.numpy_ref:
+        line["numpy_reference"] = numpy_reference_rates()
     emit(line)
     return 0
 
@@ -410,33 +450,52 @@ def gpu_arm(args, rank, world, local_rank):
             tau=0.8, gx=0.0, gy=-1e-5, Twall_top=0.9 * vs.cs2, Twall_bot=1.1 * vs.cs2,
             arith=oth))
         s2 = s + args.steps + 1000
-        w._count = 0
-        run_steps(3, s2)
-        w.synchronize()
-        w.collect()
-        w._metrics.clear()
-        barrier()
-        a0 = torch.cuda.Event(enable_timing=True)
-        a1 = torch.cuda.Event(enable_timing=True)
-        a0.record(w.stream)
-        run_steps(args.steps, s2 + 3)
-        a1.record(w.stream)
-        torch.cuda.synchronize()
-        ms2 = a0.elapsed_time(a1)
-        if dist is not None:
-            t = torch.tensor([ms2], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms2 = float(t.item())
+
+        def sustained(s0):
+            """Same protocol as the headline: warm-up, the same ~preload of
+            untimed steps (n_pre, identical on every rank), then K timed."""
+            w._count = 0
+            run_steps(3, s0)
+            for _ in range(0, n_pre, 10):
+                run_steps(10, s0 + 3)
+                w.synchronize()
+            w.collect()
+            w._metrics.clear()
+            barrier()
+            a0 = torch.cuda.Event(enable_timing=True)
+            a1 = torch.cuda.Event(enable_timing=True)
+            a0.record(w.stream)
+            run_steps(args.steps, s0 + 3)
+            a1.record(w.stream)
+            torch.cuda.synchronize()
+            m = a0.elapsed_time(a1)
+            if dist is not None:
+                t = torch.tensor([m], device=dev)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                m = float(t.item())
+            return m
+
+        ms2 = sustained(s2)
         k2 = (ms2 / args.steps if world == 1 else
               float(np.nanmean([m["t_bulk"] * 1e3 for m in w.metrics])))
         w._metrics.clear()
         w.tparams = keep
+        # A/B/A: the headline arithmetic again under the same protocol, so a
+        # drift of the clock between the arms shows
+        ms_again = sustained(s2 + args.steps + 2 * n_pre + 100)
+        w._metrics.clear()
         ach2 = BYTES_SITE * kern_sites / (k2 * 1e-3) / 1e9
         other = {"arith": oth, "value": round(sites * args.steps / (ms2 * 1e-3) / 1e6, 3),
                  "ms_per_step": round(ms2 / args.steps, 5),
                  "gflops_fp64": round(flops_step * args.steps / (ms2 * 1e-3) / 1e9, 2),
                  "kernel_ms": round(k2, 5), "kernel_GBps": round(ach2, 1),
                  "kernel_frac_of_hbm_peak": round(ach2 / hbm_peak, 4),
+                 "protocol": "A/B/A: each arm after the same %d untimed pre-load steps; "
+                             "headline arithmetic re-timed after this arm" % n_pre,
+                 "headline_again": {"arith": args.arith, "ms_per_step":
+                                    round(ms_again / args.steps, 5),
+                                    "value": round(sites * args.steps / (ms_again * 1e-3) / 1e6,
+                                                   3)},
                  "parity": ("bitwise = reference" if oth == "exact"
                             else "<=1e-12 relative (tests/test_gpu_parity.py)")}
 
@@ -758,6 +817,8 @@ def main():
     ap.add_argument("--preload", type=float, default=2.0, help="s of untimed load for clocks")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-e2e", dest="e2e", action="store_false")
+    ap.add_argument("--no-numpy-ref", dest="numpy_ref", action="store_false",
+                    help="--impl reference: skip timing the numpy reference package itself")
     ap.add_argument("--no-split", dest="split", action="store_false")
     ap.add_argument("--no-probe", dest="probe", action="store_false",
                     help="skip the FP64 DFMA peak probe")

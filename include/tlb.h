@@ -277,13 +277,11 @@ int tlb_ring_step(tlb_ring_t ring, const TlbField *prv, const TlbField *nxt,
 typedef struct TlbPeer *tlb_peer_t;
 /* 64-byte cudaIpcMemHandle of the allocation holding ptr, and ptr's offset */
 int tlb_ipc_handle(const void *ptr, char *out64, int64_t *offset);
-/* handles/offsets (6 each): left A, left B, left mailbox, right A, right B,
- * right mailbox; A = the buffer that is prv at even peer steps. */
-int tlb_peer_create(int device, const char *handles, const int64_t *offsets,
-                    tlb_peer_t *out);
-/* 2-D grid: 8 directions d = left, right, down, up, down-left, down-right,
- * up-left, up-right; handles/offsets hold (A, B, mailbox) per direction
- * (24 each), present[8] marks the exchanged directions (others ignored). */
+/* Neighbours across processes: 8 directions d = left, right, down, up,
+ * down-left, down-right, up-left, up-right (a 1-D X ring marks left and
+ * right only); handles/offsets hold (A, B, mailbox) per direction (24 each),
+ * A = the buffer that is prv at even peer steps; present[8] marks the
+ * exchanged directions (others ignored). */
 int tlb_peer_create2(int device, const char *handles, const int64_t *offsets,
                      const int *present, tlb_peer_t *out);
 int tlb_peer_destroy(tlb_peer_t peer);

@@ -104,7 +104,6 @@ SIGNATURES = [
     ("tlb_ring_exchange", _INT, [_P, _FP, _INT, _P, _P, _P]),
     ("tlb_ring_step", _INT, [_P, _FP, _FP, _PP, _INT, _P, _P, _P, _P, _P, _I64, _P]),
     ("tlb_ipc_handle", _INT, [_P, ctypes.c_char_p, ctypes.POINTER(_I64)]),
-    ("tlb_peer_create", _INT, [_INT, ctypes.c_char_p, _P, ctypes.POINTER(_P)]),
     ("tlb_peer_create2", _INT, [_INT, ctypes.c_char_p, _P, _P, ctypes.POINTER(_P)]),
     ("tlb_peer_destroy", _INT, [_P]),
     ("tlb_peer_create_local", _INT, [_INT, _P, _P, ctypes.POINTER(_P)]),

@@ -374,15 +374,6 @@ int tlb_peer_create2(int device, const char *handles, const int64_t *offsets,
 
 // 1-D ring: handles/offsets = left A, left B, left mailbox, right A, right B,
 // right mailbox
-int tlb_peer_create(int device, const char *handles, const int64_t *offsets, tlb_peer_t *out) {
-    char h[24 * 64] = {};
-    int64_t o[24] = {};
-    const int present[8] = {1, 1, 0, 0, 0, 0, 0, 0};
-    memcpy(h, handles, 6 * 64);
-    memcpy(o, offsets, 6 * sizeof(int64_t));
-    return tlb_peer_create2(device, h, o, present, out);
-}
-
 int tlb_peer_destroy(tlb_peer_t p) {
     if (!p) return TLB_OK;
     cudaSetDevice(p->device);

@@ -21,6 +21,11 @@ Fixtures (all float64 unless noted):
   rt_init.npz     the (rho, T) macro fields `init.rayleigh_taylor` hands to
                   `equilibrium` for RT 64x32 (init.py:45-64), captured by
                   wrapping the reference's equilibrium
+  halo.npz        face payloads of the reference RankWorker: pack_x(+/-1)
+                  on a 1-D 2-rank tile (runtime.py:199-208) and pack_y(+/-1)
+                  on a 2x2 tile (:226-235) of a random padded field, plus
+                  the fields after unpack_x / unpack_y of those payloads
+                  into a zeroed receiver (:210-224, :237-246)
   fingerprints.json  SHA-256 prefixes of w, f0 and f100 for RT 256x128 x 100
                   steps (the SURVEY §8c known answer), re-derived here
 """
@@ -251,7 +256,34 @@ def main():
     with open(os.path.join(HERE, "fingerprints.json"), "w") as fh:
         json.dump(fp, fh, indent=1)
     print(json.dumps(fp, indent=1))
+    halo()
+
+
+def halo():
+    """halo.npz: the reference's own face payload byte order."""
+    from thermolb.runtime import Fabric, RankWorker, decompose
+    vs = build_velocity_set("D2Q37")
+    p = PhysicsParams(tau=0.8, Twall_top=0.6, Twall_bot=0.8)
+    h = {}
+    for tag, Lx, Ly, Np, tiling in (("x", 14, 10, 2, "1d"), ("y", 14, 10, 4, (2, 2))):
+        tiles = decompose(Lx, Ly, Np, tiling, periodic_y=tag == "y")
+        w = RankWorker(tiles[0], vs, p, Fabric(Np))
+        rx = RankWorker(tiles[0], vs, p, Fabric(Np))
+        g = w.geom
+        w.prv.pops[...] = random_state(g, vs, seed=21 if tag == "x" else 22)
+        h[f"{tag}_field"] = w.prv.pops.copy()
+        h[f"{tag}_shape"] = np.array([tiles[0].Lx, tiles[0].Ly])
+        for sign in (1, -1):
+            pay = (w.pack_x if tag == "x" else w.pack_y)(w.prv, sign).copy()
+            h[f"{tag}_pack{'+' if sign == 1 else '-'}"] = pay
+            rx.prv.pops[...] = 0.0
+            (rx.unpack_x if tag == "x" else rx.unpack_y)(rx.prv, sign, pay)
+            h[f"{tag}_unpack{'+' if sign == 1 else '-'}"] = rx.prv.pops.copy()
+    np.savez_compressed(os.path.join(HERE, "halo.npz"), **h)
 
 
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["halo"]:
+        halo()
+    else:
+        main()

@@ -363,3 +363,37 @@ def test_randomised_configs_bitwise(vs, orc, case):
                       orc.params6(tau, gx, gy, 1.0, Tt, Tb),
                       ymode="periodic" if periodic else "walls")
     assert np.array_equal(res.populations, want), (case, Lx, Ly, Np, tiling, periodic)
+
+
+def _macro_contract(orc, vs, got, want):
+    """SURVEY §8c on (Q, Lx, Ly) blocks: f, rho and T within 1e-12 relative,
+    |du| <= 1e-12 * cs.  Returns the four worst errors."""
+    rel_f = np.max(np.abs(got - want) / np.abs(want))
+    mg, mw = orc.moments(got), orc.moments(want)
+    rel_rho = np.max(np.abs(mg[0] - mw[0]) / mw[0])
+    rel_T = np.max(np.abs(mg[3] - mw[3]) / mw[3])
+    du = np.max(np.hypot(mg[1] - mw[1], mg[2] - mw[2])) / np.sqrt(vs.cs2)
+    assert rel_f < 1e-12 and rel_rho < 1e-12 and rel_T < 1e-12 and du <= 1e-12, \
+        (rel_f, rel_rho, rel_T, du)
+    return rel_f, rel_rho, rel_T, du
+
+
+def test_c2_headline_fast_20_steps_vs_oracle(vs, orc):
+    """The bench's headline path at the bench config: C2 (1920x2048, RT,
+    walls), fast arithmetic through RankWorker.run_steps -- the two-step
+    kernel (tlb_step2_self) plus CUDA-graph replay, exactly what bench.py
+    times -- for 20 steps against the C oracle on the same f0."""
+    Lx, Ly, n = 1920, 2048, 20
+    macro = tl.init.rayleigh_taylor_macro(Lx, Ly, vs)
+    f0 = tl.equilibrium(*[torch.as_tensor(a).cuda() for a in macro], vs).cpu().numpy()
+    p = tl.PhysicsParams(tau=0.8, gy=-1e-5, Twall_top=0.9 * vs.cs2, Twall_bot=1.1 * vs.cs2,
+                         arith="fast")
+    tile = tl.decompose(Lx, Ly, 1, "1d")[0]
+    w = tl.RankWorker(tile, vs, p, tl.Fabric(1), schedule="overlapped", layout="column")
+    assert w.pairable()
+    w.load_block(torch.as_tensor(f0))
+    w.run_steps(0, n)
+    got = w.physical_block().cpu().numpy()
+    w.collect()
+    want, _ = orc.run(f0, n, orc.params6(0.8, 0.0, -1e-5, 1.0, p.Twall_top, p.Twall_bot))
+    print("C2 fast vs oracle (f, rho, T, |du|/cs):", _macro_contract(orc, vs, got, want))

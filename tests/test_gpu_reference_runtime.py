@@ -119,6 +119,59 @@ def test_pack_unpack_x_identity(d2q37):
             assert torch.equal(w0.prv.pops[l, g.Hx + g.Lx - d, :], w1.prv.pops[l, g.Hx - d, :])
 
 
+@pytest.mark.parametrize("layout", ["column", "soa", "aos"])
+def test_face_payload_bytes_match_reference(d2q37, layout):
+    """Halo payload byte order pinned to the reference: tlb_pack_x /
+    tlb_pack_y of the golden field equal the reference RankWorker's
+    pack_x / pack_y payloads (runtime.py:199-208, :226-235) bit for bit,
+    and unpacking those payloads into a zeroed tile writes exactly the
+    reference's halo cells (:210-224, :237-246).  tests/golden/halo.npz."""
+    from conftest import golden
+    h = golden("halo.npz")
+    fab = {"x": tl.Fabric(2), "y": tl.Fabric(4)}
+    for tag, Lx, Ly, Np, tiling in (("x", 14, 10, 2, "1d"), ("y", 14, 10, 4, (2, 2))):
+        tile = tl.decompose(Lx, Ly, Np, tiling, periodic_y=tag == "y")[0]
+        assert [tile.Lx, tile.Ly] == list(h[f"{tag}_shape"])
+        w = tl.RankWorker(tile, d2q37, tl.PhysicsParams(tau=0.8, Twall_top=0.6, Twall_bot=0.8),
+                          fab[tag], schedule="staged", layout=layout)
+        pack = w.pack_x if tag == "x" else w.pack_y
+        unpack = w.unpack_x if tag == "x" else w.unpack_y
+        for sign, key in ((1, "+"), (-1, "-")):
+            w.prv.pops.copy_(torch.as_tensor(h[f"{tag}_field"]))
+            pay = pack(w.prv, sign).cpu().numpy()
+            assert pay.tobytes() == h[f"{tag}_pack{key}"].tobytes(), (tag, key)
+            w.prv.pops.zero_()
+            unpack(w.prv, sign, torch.as_tensor(h[f"{tag}_pack{key}"]).cuda())
+            torch.cuda.synchronize()
+            assert np.array_equal(w.prv.pops.cpu().numpy(), h[f"{tag}_unpack{key}"]), (tag, key)
+
+
+def test_halo_from_peers_equals_pack_unpack(d2q37):
+    """tlb_halo_from_peers (the pull-side C export): one launch fills f's X
+    halos from its left and right neighbours' fields -- exactly what
+    unpack_x(pack_x(...)) of the reference's pbc_c exchange writes
+    (runtime.py:199-224), face-plan lines only, every other cell untouched."""
+    from paper_1703_00185_b200 import _lib
+    from paper_1703_00185_b200.kernels import field_desc
+    fab = tl.Fabric(3)
+    ws = [worker(t, d2q37, fab) for t in tl.decompose(24, 10, 3, "1d")]
+    for w in ws:
+        fill_sequential(w)
+    left, mid, right = ws
+    want = mid.prv.pops.clone()
+    mid.unpack_x(mid.prv, 1, left.pack_x(left.prv, 1))
+    mid.unpack_x(mid.prv, -1, right.pack_x(right.prv, -1))
+    torch.cuda.synchronize()
+    want, mid_ref = mid.prv.pops.clone(), want
+    mid.prv.pops.copy_(mid_ref)
+    _lib.check(_lib.load().tlb_halo_from_peers(field_desc(mid.prv), field_desc(left.prv),
+                                               field_desc(right.prv), _lib.stream_ptr()),
+               "halo_from_peers")
+    torch.cuda.synchronize()
+    assert torch.equal(mid.prv.pops, want)
+    assert not torch.equal(want, mid_ref)   # the halos did change
+
+
 def test_unpack_x_rejects_wrong_size(d2q37):
     """test_runtime.py:130-134."""
     w = worker(tl.decompose(16, 8, 2, "1d")[0], d2q37, tl.Fabric(2))
@@ -194,6 +247,36 @@ def test_snapshots_cadence():
                               params=tl.PhysicsParams(tau=0.9)))
     assert [s for s, _ in res.snapshots] == [2, 4]
     assert all(m.rho.shape == (8, 8) for _, m in res.snapshots)
+
+
+def test_snapshot_every_step_keeps_device_memory_flat():
+    """200 steps with a snapshot after every step: each snapshot is reduced
+    to (rho, u, T) on the device and moved to pinned host memory, so the
+    peak device memory of the run does not grow with the snapshot count
+    (the reference keeps host MacroFields, sim.py:89-90, 119-125)."""
+    import gc
+    p = tl.PhysicsParams(tau=0.8, gy=-1e-5, Twall_top=0.6, Twall_bot=0.75)
+
+    def peak(steps, every):
+        gc.collect()
+        torch.cuda.synchronize()
+        torch.cuda.reset_peak_memory_stats()
+        base = torch.cuda.memory_allocated()
+        res = tl.run(tl.SimConfig(Lx=512, Ly=512, Np=1, steps=steps, snapshot_every=every,
+                                  params=p, init="rayleigh-taylor"))
+        torch.cuda.synchronize()
+        return res, torch.cuda.max_memory_allocated() - base
+
+    res0, p0 = peak(200, 0)
+    res1, p1 = peak(200, 1)
+    res2, p2 = peak(20, 1)
+    assert [s for s, _ in res1.snapshots] == list(range(1, 201))
+    assert np.array_equal(res1.populations, res0.populations)
+    macro_bytes = 4 * 512 * 512 * 8
+    assert p1 <= p0 + 2 * macro_bytes, (p0, p1)
+    assert p1 == p2, (p1, p2)             # 200 snapshots peak like 20
+    last = res1.snapshots[-1][1]
+    assert np.array_equal(last.rho, res0.macro.rho) and np.array_equal(last.T, res0.macro.T)
 
 
 # ------------------------------------------------------ test_acceptance.py --
