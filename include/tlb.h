@@ -327,10 +327,13 @@ int tlb_pgm_image(const double *v, int64_t nx, int64_t ny, int64_t ld,
  * __launch_bounds__ minimum CTAs/SM of the fused kernel (1 = compiler's
  * choice, 4 = default, 5). */
 #define TLB_TUNE_MINBLOCKS 1
-#define TLB_TUNE_TB2_CFG 2   /* two-step kernel shape: 0 = 128 rows x 2 columns, 1 CTA/SM;
-                                1 = 64 x 2, 2 CTAs/SM; 2 = 96 x 2, 1 CTA/SM */
-#define TLB_TUNE_TB2_RUN 3   /* two-step kernel: columns per work item (default 96) */
+#define TLB_TUNE_TB2_CFG 2   /* two-step kernel shape (rows x columns per iteration,
+                                CTAs/SM): 0 = 128 x 2, 1; 1 = 64 x 2, 2 (default);
+                                2 = 96 x 2, 1; 3-6 warp-specialised variants */
+#define TLB_TUNE_TB2_RUN 3   /* two-step kernel: columns per work item (default 128) */
 int tlb_set_tuning(int key, int value);
+/* Current value of a tuning knob. */
+int tlb_get_tuning(int key, int *value);
 
 /* Diagnostics: measured FP64 FMA throughput of this GPU (flop/s, 2 per
  * DFMA), the denominator of the collide FP64 roofline. */

@@ -112,6 +112,7 @@ SIGNATURES = [
     ("tlb_peer_prime", _INT, [_P, _FP, _INT, _PP, _P, _P, _I64, _I64, _P]),
     ("tlb_pgm_image", _INT, [_P, _I64, _I64, _I64, _P, _P, _P]),
     ("tlb_set_tuning", _INT, [_INT, _INT]),
+    ("tlb_get_tuning", _INT, [_INT, ctypes.POINTER(ctypes.c_int)]),
     ("tlb_bench_dfma", _INT, [_I64, ctypes.POINTER(ctypes.c_double), _P]),
 ]
 

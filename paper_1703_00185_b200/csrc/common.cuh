@@ -66,6 +66,13 @@ __device__ __forceinline__ void count_neg_n(TlbStatus *st, unsigned n) {
     }
 }
 
+// Negatives test in one integer op per value: OR the high words; only a
+// result with the sign bit set (v < 0, -0.0 or a negative NaN) needs the
+// exact count (v < 0.0, kernels.py:227-229).
+__device__ __forceinline__ unsigned sign_or(unsigned acc, double v) {
+    return acc | (unsigned)__double2hiint(v);
+}
+
 __device__ __forceinline__ void count_neg(TlbStatus *st, const double (&f)[Q], bool active) {
     unsigned n = 0;
     if (active) {

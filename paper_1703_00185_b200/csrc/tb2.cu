@@ -78,7 +78,7 @@ struct RingPut {
     double (&a)[Q];
     double *row;           // ring + this thread's row
     const int (&ws)[7];    // write slot per c_x group
-    unsigned neg;
+    unsigned sgn;          // OR of the outputs' high words (sign_or)
     __device__ __forceinline__ double get(int l) const { return a[l]; }
     __device__ __forceinline__ void put(int l, double v) {
         switch (l) {
@@ -91,20 +91,51 @@ struct RingPut {
             TLB_RP(36)
 #undef TLB_RP
         }
-        neg += (unsigned)(v < 0.0);
+        sgn = sign_or(sgn, v);
     }
+    // exact count of outputs < 0, re-read from the ring only when a sign bit
+    // was seen
+    __device__ __forceinline__ unsigned negatives() const {
+        return (int)sgn >= 0 ? 0u : count_slow();
+    }
+    __device__ __forceinline__ unsigned count_slow() const;
 };
+
+template <int ROWS, int LANES>
+__device__ __forceinline__ unsigned RingPut<ROWS, LANES>::count_slow() const {
+    unsigned n = 0;
+#define TLB_RG(L) n += row[slot_of<LANES, L>(ws) * ROWS] < 0.0;
+    TLB_RG(0) TLB_RG(1) TLB_RG(2) TLB_RG(3) TLB_RG(4) TLB_RG(5) TLB_RG(6) TLB_RG(7)
+    TLB_RG(8) TLB_RG(9) TLB_RG(10) TLB_RG(11) TLB_RG(12) TLB_RG(13) TLB_RG(14)
+    TLB_RG(15) TLB_RG(16) TLB_RG(17) TLB_RG(18) TLB_RG(19) TLB_RG(20) TLB_RG(21)
+    TLB_RG(22) TLB_RG(23) TLB_RG(24) TLB_RG(25) TLB_RG(26) TLB_RG(27) TLB_RG(28)
+    TLB_RG(29) TLB_RG(30) TLB_RG(31) TLB_RG(32) TLB_RG(33) TLB_RG(34) TLB_RG(35)
+    TLB_RG(36)
+#undef TLB_RG
+    return n;
+}
 
 // level-2 outputs stream to HBM
 struct GlobalPut {
     double (&a)[Q];
     char *dp;
     const long long *doffb;
-    unsigned neg;
+    unsigned sgn;
     __device__ __forceinline__ double get(int l) const { return a[l]; }
     __device__ __forceinline__ void put(int l, double v) {
         *reinterpret_cast<double *>(dp + doffb[l]) = v;
-        neg += (unsigned)(v < 0.0);
+        sgn = sign_or(sgn, v);
+    }
+    __device__ __forceinline__ unsigned negatives() const {
+        return (int)sgn >= 0 ? 0u : count_slow();
+    }
+    // exact count, re-read from the thread's own stores (coherent loads)
+    __device__ __forceinline__ unsigned count_slow() const {
+        unsigned n = 0;
+#pragma unroll 1
+        for (int l = 0; l < Q; ++l)
+            n += *reinterpret_cast<const volatile double *>(dp + doffb[l]) < 0.0;
+        return n;
     }
 };
 
@@ -228,7 +259,7 @@ __global__ void __launch_bounds__(ROWS * LANES, MINB) k_tb2(const __grid_constan
                 RingPut<ROWS, LANES> rp{f, row, ws, 0u};
                 bits |= EXACT ? collide_exact<4>(rp, T.P) : collide_fast<4>(rp, T.P);
                 if (bits) report(T.st1, bits, xs, y1s, T.step);
-                if (row2 && X1 >= xa && X1 < xb) neg1 += rp.neg;
+                if (row2 && X1 >= xa && X1 < xb) neg1 += rp.negatives();
             }
             // the next level-1 column's HBM gather, in flight during level 2
             if (row1 && k + 1 < K && X1 + LANES < xb + 3) gather0(f, T, wrapx(X1 + LANES), y1s);
@@ -245,7 +276,7 @@ __global__ void __launch_bounds__(ROWS * LANES, MINB) k_tb2(const __grid_constan
                 GlobalPut gp{g, dp, T.doffb, 0u};
                 bits |= EXACT ? collide_exact<4>(gp, T.P) : collide_fast<4>(gp, T.P);
                 if (bits) report(T.st2, bits, X2, y1, T.step + 1);
-                neg2 += gp.neg;
+                neg2 += gp.negatives();
             }
 #pragma unroll
             for (int c = -3; c <= 3; ++c) {
@@ -369,7 +400,7 @@ __global__ void __launch_bounds__(ROWS * (PL + CL), MINB) k_tb2ws(const __grid_c
                     RingPut<ROWS, LANES> rp{f, row, wsl, 0u};
                     bits |= EXACT ? collide_exact<4>(rp, T.P) : collide_fast<4>(rp, T.P);
                     if (bits) report(T.st1, bits, wrapx(X1), y1s, T.step);
-                    if (own_row && X1 >= xa && X1 < xb) neg1 += rp.neg;
+                    if (own_row && X1 >= xa && X1 < xb) neg1 += rp.negatives();
                 }
                 const long long g = gj + j;
                 mb_arrive(&full[g % NBAR]);
@@ -396,7 +427,7 @@ __global__ void __launch_bounds__(ROWS * (PL + CL), MINB) k_tb2ws(const __grid_c
                     GlobalPut gp{g2, dp, T.doffb, 0u};
                     bits |= EXACT ? collide_exact<4>(gp, T.P) : collide_fast<4>(gp, T.P);
                     if (bits) report(T.st2, bits, X2, y1, T.step + 1);
-                    neg2 += gp.neg;
+                    neg2 += gp.negatives();
                 }
                 const long long g = gm + m;
                 mb_arrive(&empty[g % NBAR]);

@@ -55,7 +55,7 @@ static int g_minb = 4;    // tuning: __launch_bounds__ min blocks of the fused k
 // columns per iteration, 2 CTAs per SM, runs of 128 columns -- measured
 // best on B200 (tools/tb2_probe.py, profiles/r02_tb2.md)
 static int g_tb2_cfg = 1;
-static int g_tb2_run = 128;
+static int g_tb2_run = 128;      // two-step kernel: columns per work item
 static unsigned *g_tb2_ctr[64];  // two-step work-item counters (one u32 per device)
 
 // A launch covers an interior rectangle (plain gather: no halo remapping,
@@ -135,17 +135,29 @@ struct RegStoreF {
     char *dp;
     const long long *doffb;
     bool active;
-    unsigned neg;
+    unsigned sgn;          // OR of the outputs' high words (sign_or)
     __device__ __forceinline__ double get(int l) const { return a[l]; }
     __device__ __forceinline__ void put(int l, double v) {
-        // predicated store, branch-free count (no reconvergence per output)
+        // predicated store; the negatives test is one OR per output
         double *p = reinterpret_cast<double *>(dp + doffb[l]);
         if constexpr (STREAM) {
             if (active) __stcs(p, v);
         } else {
             if (active) *p = v;
         }
-        neg += (unsigned)(active & (v < 0.0));
+        sgn = sign_or(sgn, v);
+    }
+    // exact count of outputs < 0: only a site with a sign bit set among its
+    // outputs re-reads them (its own stores: plain coherent loads)
+    __device__ __forceinline__ unsigned negatives() const {
+        return (active && (int)sgn < 0) ? count_slow() : 0u;
+    }
+    __device__ __forceinline__ unsigned count_slow() const {
+        unsigned n = 0;
+#pragma unroll 1
+        for (int l = 0; l < Q; ++l)
+            n += *reinterpret_cast<const volatile double *>(dp + doffb[l]) < 0.0;
+        return n;
     }
 };
 
@@ -181,7 +193,7 @@ __device__ __forceinline__ void site_body(const SiteLaunch &L, int x, int y, boo
         RegStoreF<false> sf{f, dp, L.doffb, active, 0u};
         bits |= EXACT ? collide_exact<ORDER>(sf, L.P) : collide_fast<ORDER>(sf, L.P);
         if (active) report(L.status, bits, x, y, L.step);
-        if (L.flags & TLB_F_COUNT_NEG) count_neg_n(L.status, sf.neg);
+        if (L.flags & TLB_F_COUNT_NEG) count_neg_n(L.status, sf.negatives());
         return;
     }
     if (KIND == K_COLLIDE || KIND == K_FUSED) {
@@ -601,6 +613,15 @@ int tlb_set_tuning(int key, int value) {
     return fail(TLB_ERR_CONTRACT, "unknown tuning key %d", key);
 }
 
+int tlb_get_tuning(int key, int *value) {
+    if (!value) return fail(TLB_ERR_CONTRACT, "null value pointer");
+    if (key == TLB_TUNE_TB2_CFG) *value = g_tb2_cfg;
+    else if (key == TLB_TUNE_TB2_RUN) *value = g_tb2_run;
+    else if (key == TLB_TUNE_MINBLOCKS) *value = g_minb;
+    else return fail(TLB_ERR_CONTRACT, "unknown tuning key %d", key);
+    return TLB_OK;
+}
+
 const char *tlb_last_error(void) { return g_msg.c_str(); }
 
 int tlb_set_device(int device) {
@@ -850,6 +871,12 @@ int tlb_step2_self(const TlbField *prv, const TlbField *nxt, const TlbParams *p,
                           ((long long)CX(l) * T.src.sx + (long long)CY(l) * T.src.sy));
         T.doffb[l] = 8 * (long long)l * T.dst.sl;
     }
+    T.st1 = status1;
+    T.st2 = status2;
+    T.step = step;
+    int dev = 0, sms = 0;
+    TLB_CUDA_CHECK(cudaGetDevice(&dev));
+    TLB_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     const int hs = tb2_rows(g_tb2_cfg) - 6;     // output rows per strip, at most
     T.ns = (prv->Ly + hs - 1) / hs;
     // work items: runs of run_l columns of a strip; wall strips (bc rows)
@@ -863,12 +890,6 @@ int tlb_step2_self(const TlbField *prv, const TlbField *nxt, const TlbParams *p,
     T.hruns = (Lx + T.run_h - 1) / T.run_h;
     T.lruns = (Lx + T.run_l - 1) / T.run_l;
     T.items = (long long)T.nheavy * T.hruns + (long long)nlight * T.lruns;
-    T.st1 = status1;
-    T.st2 = status2;
-    T.step = step;
-    int dev = 0, sms = 0;
-    TLB_CUDA_CHECK(cudaGetDevice(&dev));
-    TLB_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     if (!g_tb2_ctr[dev]) TLB_CUDA_CHECK(cudaMalloc(&g_tb2_ctr[dev], sizeof(unsigned)));
     T.ctr = g_tb2_ctr[dev];
     TLB_CUDA_CHECK(cudaMemsetAsync(T.ctr, 0, sizeof(unsigned), (cudaStream_t)stream));

@@ -98,6 +98,44 @@ def test_step2_exact_bitwise_vs_oracle(orc, shape):
     assert all(s.flags == 0 for s in stat)
 
 
+@pytest.fixture
+def tb2_tuning():
+    """Restores the two-step kernel's shape and run length after a test."""
+    lib = _lib.load()
+    saved = []
+    for key in (2, 3):
+        v = ctypes.c_int(0)
+        _lib.check(lib.tlb_get_tuning(key, ctypes.byref(v)), "get_tuning")
+        saved.append((key, v.value))
+    yield lib
+    for key, v in saved:
+        _lib.check(lib.tlb_set_tuning(key, v), "set_tuning")
+
+
+@pytest.mark.parametrize("cfg", range(7))
+def test_step2_every_shape_config_bitwise(orc, tb2_tuning, cfg):
+    """Every compiled two-step kernel shape (rows x columns, CTAs/SM,
+    warp-specialised) and work items from 8 columns to whole strips: exact
+    bitwise vs the oracle."""
+    lib = tb2_tuning
+    _lib.check(lib.tlb_set_tuning(2, cfg), "cfg")
+    for (Lx, Ly, init, periodic), run in (((256, 128, "rt", False), 24),
+                                          ((256, 128, "rt", False), 8),
+                                          ((40, 245, "random", True), 9),
+                                          ((40, 245, "random", True), 100000),
+                                          ((96, 300, "random", False), 40)):
+        _lib.check(lib.tlb_set_tuning(3, run), "run")
+        vs, g, prv, nxt, f0 = _setup(Lx, Ly, init, periodic)
+        p = _params(vs, "exact")
+        got, stat = _run2(vs, g, prv, nxt, p, periodic, 4)
+        orc.set_stencil(vs.c, vs.w, vs.cs2)
+        want, neg = orc.run(f0, 4, orc.params6(p.tau, p.gx, p.gy, p.dt, p.Twall_top,
+                                               p.Twall_bot),
+                            ymode="periodic" if periodic else "walls")
+        assert np.array_equal(got, want), (cfg, Lx, Ly)
+        assert [int(s.negatives) for s in stat] == [int(v) for v in np.asarray(neg)[:4]]
+
+
 @pytest.mark.parametrize("layout", ["column", "soa", "aos"])
 def test_step2_equals_single_steps(layout):
     """Two steps in one launch == two fused launches, bitwise, for every
