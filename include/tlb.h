@@ -330,7 +330,8 @@ int tlb_pgm_image(const double *v, int64_t nx, int64_t ny, int64_t ld,
 #define TLB_TUNE_TB2_CFG 2   /* two-step kernel shape (rows x columns per iteration,
                                 CTAs/SM): 0 = 128 x 2, 1; 1 = 64 x 2, 2 (default);
                                 2 = 96 x 2, 1; 3-6 warp-specialised variants */
-#define TLB_TUNE_TB2_RUN 3   /* two-step kernel: columns per work item (default 128) */
+#define TLB_TUNE_TB2_RUN 3   /* two-step kernel: columns per work item (0 = chosen
+                                per lattice to fill whole waves; default) */
 int tlb_set_tuning(int key, int value);
 /* Current value of a tuning knob. */
 int tlb_get_tuning(int key, int *value);

@@ -51,11 +51,11 @@ static int launch_check(const char *what) {
 
 static bool g_stencil_set[64];
 static int g_minb = 4;    // tuning: __launch_bounds__ min blocks of the fused kernel
-// two-step kernel (tb2.cu) shape and work-item length: 64-row strips, 2
-// columns per iteration, 2 CTAs per SM, runs of 128 columns -- measured
-// best on B200 (tools/tb2_probe.py, profiles/r02_tb2.md)
+// two-step kernel (tb2.cu) shape: 64-row strips, 2 columns per iteration,
+// 2 CTAs per SM -- measured best on B200 (tools/tb2_probe.py,
+// profiles/r02_tb2.md); work-item length: tb2_run_length
 static int g_tb2_cfg = 1;
-static int g_tb2_run = 128;      // two-step kernel: columns per work item
+static int g_tb2_run = 0;        // two-step kernel: columns per work item (0: auto)
 static unsigned *g_tb2_ctr[64];  // two-step work-item counters (one u32 per device)
 
 // A launch covers an interior rectangle (plain gather: no halo remapping,
@@ -600,7 +600,8 @@ int tlb_set_tuning(int key, int value) {
         return TLB_OK;
     }
     if (key == TLB_TUNE_TB2_RUN) {
-        if (value < 8) return fail(TLB_ERR_CONTRACT, "two-step run must be >= 8 columns");
+        if (value != 0 && value < 8)
+            return fail(TLB_ERR_CONTRACT, "two-step run must be 0 (auto) or >= 8 columns");
         g_tb2_run = value;
         return TLB_OK;
     }
@@ -716,6 +717,9 @@ int tlb_set_stencil(int device, const int64_t *c, const double *w, double cs2) {
     TLB_CUDA_CHECK(cudaDeviceSynchronize());  // no kernel may still read the old table
     TLB_CUDA_CHECK(cudaMemcpyToSymbol(C, &h, sizeof h));
     TLB_CUDA_CHECK(tb2_set_const(h));   // the two-step kernel's copy (tb2.cu)
+    // the two-step kernel's work counter: allocated here, never inside a
+    // launch (a launch may be captured into a CUDA graph)
+    if (!g_tb2_ctr[device]) TLB_CUDA_CHECK(cudaMalloc(&g_tb2_ctr[device], sizeof(unsigned)));
     int e = set_generic(device, Q, c, w, cs2);
     if (e) return e;
     TLB_CUDA_CHECK(cudaDeviceSynchronize());
@@ -839,6 +843,32 @@ int tlb_step_self(const TlbField *prv, const TlbField *nxt, const TlbParams *p, 
     return tlb_fused(prv, nxt, r, p, flags, status, stream);
 }
 
+// Run length of the two-step kernel's work items.  The dynamic schedule
+// finishes in ceil(items / CTAs) waves of about (run + 6) columns each (the
+// 6 warm-up columns of a run), so pick the run that minimises that product
+// (C2: 15 runs of 128 = 570 items on 296 CTAs, 1.93 waves; 16 runs of 120
+// would be 608 items, 3 waves).  An explicit TLB_TUNE_TB2_RUN overrides.
+static int tb2_run_length(int Lx, int ns, bool walls, int ctas) {
+    if (g_tb2_run > 0) return g_tb2_run < Lx ? g_tb2_run : Lx;
+    const int nheavy = walls ? (ns >= 2 ? 2 : 1) : 0;
+    long long best = -1;
+    int best_run = Lx < 128 ? Lx : 128;
+    for (int r = 1; r <= Lx / 32 + 1; ++r) {
+        const int run = (Lx + r - 1) / r;
+        if (run < 32 && r > 1) break;
+        const int run_h = run / 2 > 8 ? run / 2 : run;
+        const long long items = (long long)nheavy * ((Lx + run_h - 1) / run_h) +
+                                (long long)(ns - nheavy) * r;
+        const long long waves = (items + ctas - 1) / ctas;
+        const long long cost = waves * (run + 6);
+        if (best < 0 || cost < best) {
+            best = cost;
+            best_run = run;
+        }
+    }
+    return best_run;
+}
+
 int tlb_step2_self(const TlbField *prv, const TlbField *nxt, const TlbParams *p, int walls,
                    int periodic_y, int count_neg, TlbStatus *status1, TlbStatus *status2,
                    int step, tlb_stream_t stream) {
@@ -882,7 +912,10 @@ int tlb_step2_self(const TlbField *prv, const TlbField *nxt, const TlbParams *p,
     // work items: runs of run_l columns of a strip; wall strips (bc rows)
     // first, in runs of half the length
     const int Lx = prv->Lx;
-    T.run_l = g_tb2_run < Lx ? g_tb2_run : Lx;
+    int dev0 = 0, sms0 = 0;
+    TLB_CUDA_CHECK(cudaGetDevice(&dev0));
+    TLB_CUDA_CHECK(cudaDeviceGetAttribute(&sms0, cudaDevAttrMultiProcessorCount, dev0));
+    T.run_l = tb2_run_length(Lx, T.ns, walls != 0, sms0 * (g_tb2_cfg == 1 ? 2 : 1));
     T.run_h = T.run_l / 2 > 8 ? T.run_l / 2 : T.run_l;
     T.nheavy = walls ? (T.ns >= 2 ? 2 : 1) : 0;
     T.first_light = walls ? 1 : 0;
@@ -890,7 +923,7 @@ int tlb_step2_self(const TlbField *prv, const TlbField *nxt, const TlbParams *p,
     T.hruns = (Lx + T.run_h - 1) / T.run_h;
     T.lruns = (Lx + T.run_l - 1) / T.run_l;
     T.items = (long long)T.nheavy * T.hruns + (long long)nlight * T.lruns;
-    if (!g_tb2_ctr[dev]) TLB_CUDA_CHECK(cudaMalloc(&g_tb2_ctr[dev], sizeof(unsigned)));
+    if (!g_tb2_ctr[dev]) return fail(TLB_ERR_STENCIL, "stencil not set on device %d", dev);
     T.ctr = g_tb2_ctr[dev];
     TLB_CUDA_CHECK(cudaMemsetAsync(T.ctr, 0, sizeof(unsigned), (cudaStream_t)stream));
     TLB_CUDA_CHECK(tb2_launch(T, p->arith == TLB_ARITH_EXACT, g_tb2_cfg, sms, (cudaStream_t)stream));

@@ -749,12 +749,17 @@ class RankWorker:
         return (self.x_self and not self.y_exchange and self._ring is None
                 and self._peer is None and not self.debug_poison and self.timing != "every")
 
+    # "auto" pairs steps only on tiles this large: the two-step kernel needs
+    # enough strip runs to fill the GPU (1024x2048: 12.7k vs 10.6k MLUPS for
+    # the single step; 256x128: 270 vs 3,200; profiles/r02_tb2.md)
+    PAIR_MIN_SITES = 2_000_000
+
     def pairable(self):
         """Two steps per launch (temporal blocking, csrc/tb2.cu): a single
         self-periodic tile with the overlapped schedule, D2Q37 order 4, at
-        least 8x8.  "auto" takes it for the fast arithmetic (where it is the
-        faster kernel); "on" for both arithmetics; results are the same bits
-        as two single steps either way."""
+        least 8x8.  "auto" takes it for the fast arithmetic on large tiles
+        (where it is the faster kernel); "on" for both arithmetics and any
+        size; results are the same bits as two single steps either way."""
         if self.temporal == "off" or self.schedule != "overlapped" or self.debug_poison:
             return False
         order = self.params.eq_order if self.params.eq_order is not None else self.vs.eq_order
@@ -762,7 +767,8 @@ class RankWorker:
                 and (self.y_self or (self.wall_bot and self.wall_top))
                 and self.vs.Q == 37 and order == 4 and self.geom.Lx >= 8 and self.geom.Ly >= 8):
             return False
-        return self.temporal == "on" or self.tparams.arith == _lib.ARITH["fast"]
+        return self.temporal == "on" or (self.tparams.arith == _lib.ARITH["fast"] and
+                                         self.geom.Lx * self.geom.Ly >= self.PAIR_MIN_SITES)
 
     def step_pair(self, step_no):
         """Steps step_no and step_no + 1 in ONE launch (tlb_step2_self): the

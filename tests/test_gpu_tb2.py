@@ -212,16 +212,32 @@ def test_run_uses_pairs_bitwise(orc, periodic):
         assert np.array_equal(m.ux, ux) and np.array_equal(m.uy, uy)
 
 
-def test_run_fast_default_pairs_within_contract(orc):
-    """The default for fast arithmetic on one tile is two steps per launch:
-    f, rho and T within 1e-12 relative, |du| <= 1e-12 cs after 100 steps."""
+def test_pairing_policy():
+    """"auto" pairs steps for the fast arithmetic on large tiles only (the
+    two-step kernel needs ~2 waves of strip runs to win, profiles/r02_tb2.md);
+    "on" pairs any tile and both arithmetics; exact stays single-step."""
+    vs = tl.build_velocity_set("D2Q37")
+    fast = tl.PhysicsParams(tau=0.8, Twall_top=0.6, Twall_bot=0.7, arith="fast")
+    exact = tl.PhysicsParams(tau=0.8, Twall_top=0.6, Twall_bot=0.7)
+
+    def w(Lx, Ly, p, **kw):
+        return tl.RankWorker(tl.decompose(Lx, Ly, 1, "1d")[0], vs, p, tl.Fabric(1),
+                             schedule="overlapped", **kw)
+    assert w(1920, 2048, fast).pairable()
+    assert not w(256, 128, fast).pairable()
+    assert not w(1920, 2048, exact).pairable()
+    assert w(256, 128, exact, temporal="on").pairable()
+    assert not w(1920, 2048, fast, temporal="off").pairable()
+
+
+def test_run_fast_pairs_within_contract(orc):
+    """Fast arithmetic, two steps per launch through run(): f, rho and T
+    within 1e-12 relative, |du| <= 1e-12 cs after 100 steps."""
     vs = tl.build_velocity_set("D2Q37")
     p = tl.PhysicsParams(tau=0.8, gy=-1e-5, Twall_top=0.9 * vs.cs2, Twall_bot=1.1 * vs.cs2,
                          arith="fast")
-    w = tl.RankWorker(tl.decompose(64, 48, 1, "1d")[0], vs, p, tl.Fabric(1),
-                      schedule="overlapped")
-    assert w.pairable()
-    res = tl.run(tl.SimConfig(Lx=256, Ly=128, steps=100, params=p, init="rayleigh-taylor"))
+    res = tl.run(tl.SimConfig(Lx=256, Ly=128, steps=100, params=p, init="rayleigh-taylor",
+                              temporal="on"))
     orc.set_stencil(vs.c, vs.w, vs.cs2)
     f0 = orc.equilibrium(*orc.rayleigh_taylor_macro(256, 128, vs.cs2))
     want, _ = orc.run(f0, 100, orc.params6(p.tau, p.gx, p.gy, p.dt, p.Twall_top, p.Twall_bot))
@@ -231,3 +247,23 @@ def test_run_fast_default_pairs_within_contract(orc):
     assert np.max(np.abs(res.macro.T - T) / T) < 1e-12
     du = np.hypot(res.macro.ux - ux, res.macro.uy - uy)
     assert np.max(du) <= 1e-12 * np.sqrt(vs.cs2)
+
+
+def test_first_pair_launch_inside_graph_capture():
+    """A fresh process whose first two-step launch is captured into a CUDA
+    graph (run() with temporal="on" and >= 32 steps): the launch allocates
+    nothing (the work counter is set up with the stencil)."""
+    import subprocess
+    import sys
+    code = ("import paper_1703_00185_b200 as tl\n"
+            "vs = tl.build_velocity_set('D2Q37')\n"
+            "p = tl.PhysicsParams(tau=0.8, Twall_top=0.9 * vs.cs2, Twall_bot=1.1 * vs.cs2)\n"
+            "r = tl.run(tl.SimConfig(Lx=64, Ly=48, steps=64, params=p, init='rayleigh-taylor',"
+            " temporal='on'))\n"
+            "print('ok', len(r.metrics))\n")
+    import os
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True,
+                         timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert "ok 64" in out.stdout

@@ -27,7 +27,8 @@ def main():
     ap.add_argument("--arith", default="fast,exact")
     ap.add_argument("--preload", type=float, default=2.0)
     ap.add_argument("--cfg", default="1", help="two-step kernel shapes to try (TLB_TUNE_TB2_CFG)")
-    ap.add_argument("--run", default="128", help="columns per work item (TLB_TUNE_TB2_RUN)")
+    ap.add_argument("--run", default="0",
+                    help="columns per work item (TLB_TUNE_TB2_RUN, 0 = auto)")
     a = ap.parse_args()
     vs = tl.build_velocity_set("D2Q37")
     _lib.ensure_stencil(vs, 0)
