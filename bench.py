@@ -350,7 +350,7 @@ def gpu_arm(args, rank, world, local_rank):
     # one tile (N=1): two steps per launch where it applies (temporal
     # blocking, csrc/tb2.cu; RankWorker.pairable) -- run()'s own path
     def run_steps(n, s0=0):
-        pair = world == 1 and w.pairable()
+        pair = w.pairable()
         s = s0
         while s < s0 + n:
             if pair and s + 1 < s0 + n:
@@ -417,12 +417,15 @@ def gpu_arm(args, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     metrics = w.metrics
-    pair = world == 1 and w.pairable()
+    pair = w.pairable()
     launches = args.steps // 2 + args.steps % 2 if pair else args.steps
     # N=1: the region holds only the step launches: per-launch time = region
     # / launches (a two-step launch counts as two steps' worth)
+    # N>1: t_bulk of a sampled launch (a pair launch reports half its time
+    # per step: twice that is the launch)
     bulk_ms = ([ms * (2.0 if pair else 1.0) / args.steps] if world == 1 else
-               [m["t_bulk"] * 1e3 for m in metrics if m["t_bulk"] == m["t_bulk"]])
+               [m["t_bulk"] * 1e3 * (2.0 if pair else 1.0) for m in metrics
+                if m["t_bulk"] == m["t_bulk"]])
     sites = Lx * Ly
     mlups = sites * args.steps / (ms * 1e-3) / 1e6
     flops_step = FLOP_SITE * sites + FLOP_WALL_SITE * 6 * Lx
@@ -431,7 +434,7 @@ def gpu_arm(args, rank, world, local_rank):
     # dominant kernel: the fused step over the (bulk) region of this rank
     h = 3
     ey = (2 * h if grid[1] > 1 else 0)    # rows of exchanged Y edges (2-D), approx.
-    kern_sites = (Lx_tile if world == 1 else Lx_tile - 2 * h) * (Ly_tile - ey)
+    kern_sites = (Lx_tile if world == 1 or pair else Lx_tile - 2 * h) * (Ly_tile - ey)
     kern_ms = float(np.mean(bulk_ms))
     achieved = BYTES_SITE * kern_sites / (kern_ms * 1e-3) / 1e9
     pk = peaks()
@@ -500,7 +503,8 @@ def gpu_arm(args, rank, world, local_rank):
                             else "<=1e-12 relative (tests/test_gpu_parity.py)")}
 
     w.timing = "sampled"
-    kname = ("k_tb2<%d, 64, 2, 2>" % (1 if args.arith == "exact" else 0) if pair else
+    kname = ("k_tb2<%d, 64, 2, 2>" % (1 if args.arith == "exact" else 0) if pair and world == 1
+             else "k_tb2<%d, 64, 2, 2, 1>" % (1 if args.arith == "exact" else 0) if pair else
              "k_site<3, %d, 4, 0, 4>" % (1 if args.arith == "exact" else 0) if world == 1 else
              "k_peer_step<%d, 0>" % (1 if args.arith == "exact" else 0))
     traffic, traffic_src = ncu_traffic(kname, args.layout)

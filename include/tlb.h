@@ -294,8 +294,9 @@ int tlb_peer_create_local(int device, void *const *ptrs, const int *present,
  * passes its fabric timeout (SimConfig.recv_timeout, sim.py:40). */
 int tlb_peer_set_timeout(tlb_peer_t peer, double seconds);
 /* One step.  nxt_index: 0 if nxt is buffer A, 1 if B.  mailbox: this rank's
- * zeroed device mailbox of >= 10 u64 ([0..7] value published by the
- * neighbour in direction d, [8] border-block counter, [9] sticky failure).
+ * zeroed device mailbox of >= 11 u64 ([0..7] value published by the
+ * neighbour in direction d, [8] border-block counter, [9] sticky failure, [10]
+ * the two-step ring kernel's work counter).
  * peer_step: 0, 1, 2, ... (border blocks wait for mailbox count >=
  * peer_step).  step_tag: the step number, published with the step and
  * checked against the neighbours' (TLB_ST_PROTOCOL on a mismatch, the
@@ -315,6 +316,25 @@ int tlb_peer_prime(tlb_peer_t peer, const TlbField *prv, int prv_index,
                    const TlbParams *p, TlbStatus *status,
                    unsigned long long *mailbox, int64_t peer_step,
                    int64_t step_tag, tlb_stream_t stream);
+
+/* Two time steps per launch on a 1-D X ring (temporal blocking across
+ * GPUs): the step-pair kernel of tlb_step2_self whose border runs read 6-column
+ * X halos (prv->Hx >= 6) and store their own 6 border columns of the second
+ * step into the neighbours' nxt halos (NVLink stores), with the mailbox
+ * protocol of tlb_peer_step (one launch = one peer step; step_tag = the
+ * first of the two steps; a neighbour's previous launch must have ended at
+ * step_tag - 1).  Left and right neighbours only; Lx >= 12.  status1 /
+ * status2: steps step_tag and step_tag + 1. */
+int tlb_peer_step2(tlb_peer_t peer, const TlbField *prv, const TlbField *nxt,
+                   int nxt_index, const TlbParams *p, int flags, TlbStatus *status1,
+                   TlbStatus *status2, unsigned long long *mailbox, int64_t peer_step,
+                   int64_t step_tag, int check_prev, tlb_stream_t stream);
+/* Halo fill for tlb_peer_step2 (6 columns deep) before its first launch
+ * after a (re)load or after single steps; counts as a peer step published
+ * as step step_tag. */
+int tlb_peer_prime2(tlb_peer_t peer, const TlbField *prv, int prv_index,
+                    const TlbParams *p, TlbStatus *status, unsigned long long *mailbox,
+                    int64_t peer_step, int64_t step_tag, tlb_stream_t stream);
 
 /* Snapshot image (io.write_pgm, io.py:13-24): min-max normalised 8-bit
  * quantisation of a (nx, ny) field with row stride ld into img (nx*ny bytes,

@@ -110,6 +110,8 @@ SIGNATURES = [
     ("tlb_peer_set_timeout", _INT, [_P, ctypes.c_double]),
     ("tlb_peer_step", _INT, [_P, _FP, _FP, _INT, _PP, _INT, _P, _P, _I64, _I64, _INT, _P]),
     ("tlb_peer_prime", _INT, [_P, _FP, _INT, _PP, _P, _P, _I64, _I64, _P]),
+    ("tlb_peer_step2", _INT, [_P, _FP, _FP, _INT, _PP, _INT, _P, _P, _P, _I64, _I64, _INT, _P]),
+    ("tlb_peer_prime2", _INT, [_P, _FP, _INT, _PP, _P, _P, _I64, _I64, _P]),
     ("tlb_pgm_image", _INT, [_P, _I64, _I64, _I64, _P, _P, _P]),
     ("tlb_set_tuning", _INT, [_INT, _INT]),
     ("tlb_get_tuning", _INT, [_INT, ctypes.POINTER(ctypes.c_int)]),

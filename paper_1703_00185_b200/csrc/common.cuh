@@ -6,7 +6,39 @@
 #include "../../include/tlb.h"
 #include "d2q37.cuh"
 
+// ------------------------------------------------- peer mailbox protocol --
+// (tlb_peer.cuh: the single-step ring; tb2.cu: the two-step ring)
+// Default bound of the border blocks' wait; tlb_peer_set_timeout sets it per
+// peer object (the host passes its fabric timeout).
+#define TLB_PEER_TIMEOUT_NS 5000000000ull
+
+// mailbox layout (u64): [0..7] value published by the neighbour in direction
+// d, [8] border-block counter, [9] sticky failure flag, [10] work counter.  A published value
+// carries the neighbour's step count (bits 0..39), the step tag = its step
+// number + 1 (bits 40..62; runtime.py:151-154's step check) and, in bit 63,
+// "I failed" (a timed-out rank poisons what it publishes, so its neighbours
+// stop too instead of using halos that were never written).
+#define TLB_MB_COUNTER 8
+#define TLB_MB_STICKY 9
+#define TLB_MB_WORK 10     /* the ring two-step kernel's work-item counter */
+#define TLB_MB_CTR_MASK ((1ull << 40) - 1)
+#define TLB_MB_TAG_SHIFT 40
+#define TLB_MB_TAG_MASK ((1ull << 23) - 1)
+#define TLB_MB_POISON (1ull << 63)
+
 namespace tlb {
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 
 // --------------------------------------------------------- device helpers --
 struct Fld {

@@ -151,18 +151,32 @@ struct RingGet {
     }
 };
 
-// level-0 gather for the level-1 site (x, y) (physical coordinates)
-__device__ __forceinline__ void gather0(double (&f)[Q], const TbLaunch &T, int x, int y) {
+// level-0 gather for the level-1 site (x, y) (padded coordinates).  XWRAP:
+// the tile is its own X neighbour (implicit periodic halo); else the X halo
+// memory is read (the ring variant's 6 columns).  coh: coherent L2 loads for
+// halos other GPUs stored while this grid may be running.
+template <bool XWRAP>
+__device__ __forceinline__ void gather0(double (&f)[Q], const TbLaunch &T, int x, int y,
+                                        bool coh = false) {
     const Fld &S = T.src;
-    const bool inner = x >= S.Hx + 3 && x < S.Hx + S.Lx - 3 && y >= S.Hy + 3 &&
+    const bool inner = (!XWRAP || (x >= S.Hx + 3 && x < S.Hx + S.Lx - 3)) && y >= S.Hy + 3 &&
                        y < S.Hy + S.Ly - 3;
     if (inner) {
         const char *sp = reinterpret_cast<const char *>(S.base + (long long)x * S.sx +
                                                         (long long)y * S.sy);
+        if (coh) {
 #pragma unroll
-        for (int l = 0; l < Q; ++l) f[l] = __ldg(reinterpret_cast<const double *>(sp + T.soffb[l]));
+            for (int l = 0; l < Q; ++l)
+                f[l] = __ldcg(reinterpret_cast<const double *>(sp + T.soffb[l]));
+        } else {
+#pragma unroll
+            for (int l = 0; l < Q; ++l)
+                f[l] = __ldg(reinterpret_cast<const double *>(sp + T.soffb[l]));
+        }
+    } else if (coh) {
+        load_all<1>(f, S, x, y, true, true, T.flags);
     } else {
-        load_all<false>(f, S, x, y, true, true, T.flags);
+        load_all<0>(f, S, x, y, true, true, T.flags);
     }
 }
 
@@ -208,7 +222,123 @@ __device__ __forceinline__ void item_of(const TbLaunch &T, long long i, int &str
     xb += T.src.Hx;
 }
 
-template <bool EXACT, int ROWS, int LANES, int MINB>
+// Ring variant: the same runs, the border runs (first and last of every
+// strip: they read the X halos and store into the neighbours) last.
+__device__ __forceinline__ void item_of_peer(const TbLaunch &T, long long i, int &strip,
+                                             int &xa, int &xb, bool &edge) {
+    const int Lx = T.src.Lx;
+    const long long hi = (long long)T.nheavy * (T.hruns - 2);
+    const long long li = (long long)(T.ns - T.nheavy) * (T.lruns - 2);
+    int rl, r;
+    edge = false;
+    if (i < hi) {
+        const int h = (int)(i / (T.hruns - 2));
+        strip = h == 0 ? 0 : T.ns - 1;
+        r = 1 + (int)(i % (T.hruns - 2));
+        rl = T.run_h;
+    } else if (i < hi + li) {
+        i -= hi;
+        strip = T.first_light + (int)(i / (T.lruns - 2));
+        r = 1 + (int)(i % (T.lruns - 2));
+        rl = T.run_l;
+    } else {
+        const long long j = i - hi - li;
+        edge = true;
+        strip = (int)(j / 2);
+        const bool heavy = T.nheavy > 0 && (strip == 0 || strip == T.ns - 1);
+        rl = heavy ? T.run_h : T.run_l;
+        const int runs = heavy ? T.hruns : T.lruns;
+        r = (j & 1) ? runs - 1 : 0;
+    }
+    xa = r * rl;
+    xb = xa + rl < Lx ? xa + rl : Lx;
+    xa += T.src.Hx;
+    xb += T.src.Hx;
+}
+
+// thread 0: wait until both neighbours have published launch need-1;
+// bit 0 = timeout / failed neighbour, bit 1 = step-tag mismatch
+__device__ __forceinline__ int tb2_peer_wait(const TbPeer &E) {
+    int fail = 0;
+    const unsigned long long t0 = globaltimer();
+    const unsigned long long need = (unsigned long long)E.need;
+    for (int d = 0; d < 2 && !(fail & 1); ++d) {
+        unsigned long long v;
+        while (((v = ld_acquire_sys(E.mb + d)) & TLB_MB_CTR_MASK) < need) {
+            if (ld_acquire_sys(E.mb + TLB_MB_STICKY) || globaltimer() - t0 > E.timeout_ns) {
+                fail |= 1;
+                break;
+            }
+            __nanosleep(256);
+        }
+        if (fail & 1) break;
+        if (v & TLB_MB_POISON) {
+            fail |= 1;
+            break;
+        }
+        // a neighbour at our count ended at step tag - 1 (published tag), one
+        // launch ahead at the end of this launch's span (tag + span)
+        const unsigned long long ctr = v & TLB_MB_CTR_MASK;
+        const unsigned long long tag = (v >> TLB_MB_TAG_SHIFT) & TLB_MB_TAG_MASK;
+        if (need > 0) {
+            if (ctr == need + 1) {
+                if (tag != ((unsigned long long)(E.tag + E.span) & TLB_MB_TAG_MASK)) fail |= 2;
+            } else if (ctr == need) {
+                if (E.check_prev && tag != ((unsigned long long)E.tag & TLB_MB_TAG_MASK))
+                    fail |= 2;
+            } else {
+                fail |= 2;
+            }
+        }
+    }
+    if (fail & 1) atomicExch(E.mb + TLB_MB_STICKY, 1ull);
+    return fail;
+}
+
+// thread 0, after the block's border work: count it; the last border block
+// publishes "launch done" (count need+1, tag = last step + 1) to both
+// neighbours (fence / counter / fence, as in tlb_peer.cuh)
+__device__ __forceinline__ void tb2_peer_done(const TbPeer &E, long long nblocks, long long tag_next) {
+    __threadfence_system();
+    if (atomicAdd(E.mb + TLB_MB_COUNTER, 1ull) != (unsigned long long)(nblocks - 1)) return;
+    E.mb[TLB_MB_COUNTER] = 0;
+    __threadfence_system();
+    unsigned long long v = ((unsigned long long)E.need + 1) |
+                           (((unsigned long long)tag_next & TLB_MB_TAG_MASK) << TLB_MB_TAG_SHIFT);
+    if (ld_acquire_sys(E.mb + TLB_MB_STICKY)) v |= TLB_MB_POISON;
+    // we are the left neighbour's right neighbour and vice versa
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(E.nbmb[0] + 1), "l"(v) : "memory");
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(E.nbmb[1] + 0), "l"(v) : "memory");
+}
+
+// level-2 outputs of a border column: also into the neighbour's halo, the
+// populations its level-1 halo sites pull (depth d from our edge: left
+// neighbour c_x <= 3 - d, right neighbour c_x >= d - 3)
+struct PeerPut {
+    double (&a)[Q];
+    char *dp;
+    const long long *doffb;
+    char *lp, *rp;         // neighbours' site addresses (or null)
+    int tl, tr;            // thresholds 3 - d (left), d - 3 (right)
+    unsigned sgn;
+    __device__ __forceinline__ double get(int l) const { return a[l]; }
+    __device__ __forceinline__ void put(int l, double v) {
+        *reinterpret_cast<double *>(dp + doffb[l]) = v;
+        if (lp && CX(l) <= tl) *reinterpret_cast<double *>(lp + doffb[l]) = v;
+        if (rp && CX(l) >= tr) *reinterpret_cast<double *>(rp + doffb[l]) = v;
+        sgn = sign_or(sgn, v);
+    }
+    __device__ __forceinline__ unsigned negatives() const {
+        if ((int)sgn >= 0) return 0u;
+        unsigned n = 0;
+#pragma unroll 1
+        for (int l = 0; l < Q; ++l)
+            n += *reinterpret_cast<const volatile double *>(dp + doffb[l]) < 0.0;
+        return n;
+    }
+};
+
+template <bool EXACT, int ROWS, int LANES, int MINB, bool PEER = false>
 __global__ void __launch_bounds__(ROWS * LANES, MINB) k_tb2(const __grid_constant__ TbLaunch T) {
     extern __shared__ double ring[];
     __shared__ long long s_item;
@@ -217,6 +347,8 @@ __global__ void __launch_bounds__(ROWS * LANES, MINB) k_tb2(const __grid_constan
     const int Lx = S.Lx, Ly = S.Ly, Hx = S.Hx, Hy = S.Hy;
     double *row = ring + r;
     unsigned neg1 = 0, neg2 = 0;
+    __shared__ int s_fail;
+    int fail = -1;           // ring variant: result of this block's one wait
     for (;;) {
         // dynamic schedule: the next work item (one strip run) for the CTA
         if (threadIdx.x == 0) s_item = (long long)atomicAdd(T.ctr, 1u);
@@ -224,7 +356,26 @@ __global__ void __launch_bounds__(ROWS * LANES, MINB) k_tb2(const __grid_constan
         const long long item = s_item;
         if (item >= T.items) break;
         int strip, xa, xb;
-        item_of(T, item, strip, xa, xb);
+        bool edge = false;
+        if constexpr (PEER) item_of_peer(T, item, strip, xa, xb, edge);
+        else item_of(T, item, strip, xa, xb);
+        if (PEER && edge && fail < 0) {
+            // first border run of this block: both neighbours' previous
+            // launch must be done (halos written, ours read)
+            if (threadIdx.x == 0) s_fail = tb2_peer_wait(T.pe);
+            __syncthreads();
+            fail = s_fail;
+            if (threadIdx.x == 0 && fail) {
+                if (fail & 1) report(T.st1, TLB_ST_PEER_TIMEOUT, xa, Hy, T.step);
+                if (fail & 2) report(T.st1, TLB_ST_PROTOCOL, xa, Hy, T.step);
+            }
+        }
+        if (PEER && edge && (fail & 1)) {
+            // a neighbour is gone: no compute, but count the run so the
+            // (poisoned) publication still happens
+            if (threadIdx.x == 0) tb2_peer_done(T.pe, T.pe.edges, T.step + 2);
+            continue;
+        }
         const int ys = Hy + (int)((long long)Ly * strip / T.ns);
         const int hs = Hy + (int)((long long)Ly * (strip + 1) / T.ns) - ys;
         // this thread's level-1 row and the physical site it stands for
@@ -239,9 +390,11 @@ __global__ void __launch_bounds__(ROWS * LANES, MINB) k_tb2(const __grid_constan
         }
         const bool row2 = r >= 3 && r < hs + 3;   // level-2 row y1 is an output row
         const int K = (xb - xa + 6 + LANES - 1) / LANES;
-        auto wrapx = [&](int x) { return x < Hx ? x + Lx : (x >= Hx + Lx ? x - Lx : x); };
+        auto wrapx = [&](int x) {
+            return PEER ? x : x < Hx ? x + Lx : (x >= Hx + Lx ? x - Lx : x);
+        };
         double f[Q];
-        if (row1) gather0(f, T, wrapx(xa - 3 + lane), y1s);
+        if (row1) gather0<!PEER>(f, T, wrapx(xa - 3 + lane), y1s, edge);
         // ring slots of level-1 column j (written) and of the columns level 2
         // reads (j - 3 - c), per c_x group; advanced by LANES per iteration
         int ws[7], rs[7];
@@ -262,7 +415,8 @@ __global__ void __launch_bounds__(ROWS * LANES, MINB) k_tb2(const __grid_constan
                 if (row2 && X1 >= xa && X1 < xb) neg1 += rp.negatives();
             }
             // the next level-1 column's HBM gather, in flight during level 2
-            if (row1 && k + 1 < K && X1 + LANES < xb + 3) gather0(f, T, wrapx(X1 + LANES), y1s);
+            if (row1 && k + 1 < K && X1 + LANES < xb + 3)
+                gather0<!PEER>(f, T, wrapx(X1 + LANES), y1s, edge);
             __syncthreads();
             const int X2 = X1 - 3;
             if (row2 && X2 >= xa && X2 < xb) {
@@ -273,10 +427,26 @@ __global__ void __launch_bounds__(ROWS * LANES, MINB) k_tb2(const __grid_constan
                 unsigned bits = walls<EXACT>(g, T, y1);
                 char *dp = reinterpret_cast<char *>(T.dst.base + (long long)X2 * T.dst.sx +
                                                     (long long)y1 * T.dst.sy);
-                GlobalPut gp{g, dp, T.doffb, 0u};
-                bits |= EXACT ? collide_exact<4>(gp, T.P) : collide_fast<4>(gp, T.P);
+                const int xp = X2 - Hx;
+                const int dl = PEER && edge && xp < 6 ? xp + 1 : 0;
+                const int dr = PEER && edge && xp >= Lx - 6 ? Lx - xp : 0;
+                if (dl || dr) {
+                    const long long off = (long long)y1 * T.dst.sy;
+                    char *lp = dl ? reinterpret_cast<char *>(
+                                        T.pe.nb[0] + (long long)(X2 + Lx) * T.dst.sx + off)
+                                  : nullptr;
+                    char *rp = dr ? reinterpret_cast<char *>(
+                                        T.pe.nb[1] + (long long)(X2 - Lx) * T.dst.sx + off)
+                                  : nullptr;
+                    PeerPut pp{g, dp, T.doffb, lp, rp, 3 - dl, dr - 3, 0u};
+                    bits |= EXACT ? collide_exact<4>(pp, T.P) : collide_fast<4>(pp, T.P);
+                    neg2 += pp.negatives();
+                } else {
+                    GlobalPut gp{g, dp, T.doffb, 0u};
+                    bits |= EXACT ? collide_exact<4>(gp, T.P) : collide_fast<4>(gp, T.P);
+                    neg2 += gp.negatives();
+                }
                 if (bits) report(T.st2, bits, X2, y1, T.step + 1);
-                neg2 += gp.negatives();
             }
 #pragma unroll
             for (int c = -3; c <= 3; ++c) {
@@ -287,6 +457,9 @@ __global__ void __launch_bounds__(ROWS * LANES, MINB) k_tb2(const __grid_constan
             }
             __syncthreads();
         }
+        // a border run's halo reads and remote stores are done (the barrier
+        // above): count it; the last one publishes
+        if (PEER && edge && threadIdx.x == 0) tb2_peer_done(T.pe, T.pe.edges, T.step + 2);
     }
     if (T.flags & TLB_F_COUNT_NEG) {
         count_neg_n(T.st1, neg1);
@@ -294,11 +467,43 @@ __global__ void __launch_bounds__(ROWS * LANES, MINB) k_tb2(const __grid_constan
     }
 }
 
-template <bool EXACT, int ROWS, int LANES, int MINB>
+// Halo fill of the ring variant before its first launch after a (re)load:
+// every rank pushes the populations of its 6 border columns of level 0 that
+// the neighbours' level-1 halo sites pull into their level-0 halos (T.pe.nb
+// = the neighbours' buffer twin of T.src), then publishes as a launch.
+__global__ void k_tb2_prime(const __grid_constant__ TbLaunch T) {
+    __shared__ int s_fail;
+    if (threadIdx.x == 0) s_fail = tb2_peer_wait(T.pe);
+    __syncthreads();
+    const Fld &S = T.src;
+    const long long n = 12LL * S.Ly;   // (side, depth) x rows
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (!(s_fail & 1) && i < n) {
+        const int side = (int)(i / (6LL * S.Ly)), d = 1 + (int)((i / S.Ly) % 6);
+        const int y = S.Hy + (int)(i % S.Ly);
+        const int x = side ? S.Hx + S.Lx - d : S.Hx + d - 1;
+        const long long so = (long long)x * S.sx + (long long)y * S.sy;
+        const long long ro = (long long)(side ? x - S.Lx : x + S.Lx) * S.sx + (long long)y * S.sy;
+        double *dst = T.pe.nb[side];
+#pragma unroll
+        for (int l = 0; l < Q; ++l) {
+            const bool need = side ? CX(l) >= d - 3 : CX(l) <= 3 - d;
+            if (need) dst[ro + (long long)l * S.sl] = S.base[so + (long long)l * S.sl];
+        }
+    }
+    if (threadIdx.x == 0 && s_fail) {
+        if (s_fail & 1) report(T.st1, TLB_ST_PEER_TIMEOUT, S.Hx, S.Hy, T.step);
+        if (s_fail & 2) report(T.st1, TLB_ST_PROTOCOL, S.Hx, S.Hy, T.step);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) tb2_peer_done(T.pe, gridDim.x, T.step + 1);
+}
+
+template <bool EXACT, int ROWS, int LANES, int MINB, bool PEER = false>
 static cudaError_t launch_cfg(const TbLaunch &T, int sms, cudaStream_t s) {
     const size_t smem = (size_t)slots(LANES) * ROWS * sizeof(double);
     static bool attr = false;
-    auto *fn = k_tb2<EXACT, ROWS, LANES, MINB>;
+    auto *fn = k_tb2<EXACT, ROWS, LANES, MINB, PEER>;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem);
@@ -387,7 +592,7 @@ __global__ void __launch_bounds__(ROWS * (PL + CL), MINB) k_tb2ws(const __grid_c
             for (int j = lane; j < NJ; j += PL) {
                 const int X1 = xa - 3 + j;
                 double f[Q];
-                if (row1) gather0(f, T, wrapx(X1), y1s);
+                if (row1) gather0<true>(f, T, wrapx(X1), y1s);
                 if (j >= E + 3) {
                     const long long m = gm + (j - E - 3);
                     mb_wait(&empty[m % NBAR], (unsigned)((m / NBAR) & 1));
@@ -467,6 +672,17 @@ cudaError_t tb2_set_const(const StencilConst &h) {
 
 int tb2_rows(int cfg) {
     return (cfg == 1 || cfg == 4) ? 64 : (cfg == 2 || cfg == 6) ? 96 : 128;
+}
+
+cudaError_t tb2_launch_peer(const tb2::TbLaunch &T, bool exact, int sms, cudaStream_t s) {
+    return exact ? tb2::launch_cfg<true, 64, 2, 2, true>(T, sms, s)
+                 : tb2::launch_cfg<false, 64, 2, 2, true>(T, sms, s);
+}
+
+cudaError_t tb2_prime_peer(const tb2::TbLaunch &T, cudaStream_t s) {
+    const long long n = 12LL * T.src.Ly;
+    tb2::k_tb2_prime<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(T);
+    return cudaGetLastError();
 }
 
 cudaError_t tb2_launch(const tb2::TbLaunch &T, bool exact, int cfg, int sms, cudaStream_t s) {

@@ -13,6 +13,25 @@ namespace tb2 {
 // of n_c (LANES + 3 + c) = 37 (LANES + 3)
 __host__ __device__ constexpr int slots(int lanes) { return 37 * (lanes + 3); }
 
+// Two steps per launch on a 1-D X ring of GPUs (tb2.cu, PEER): the border
+// runs of every strip run last, wait for both neighbours' previous launch,
+// read the 6-column halos those stored into our level-0 buffer, and store
+// their own 6 border columns of level 2 into the neighbours' level-2 buffer
+// halos (NVLink stores); the last border run publishes.
+struct TbPeer {
+    double *nb[2];                 // left, right neighbours' buffer that is our dst's twin
+    unsigned long long *nbmb[2];   // their mailboxes
+    unsigned long long *mb;        // ours
+    long long need;                // wait until both mailbox counts >= need
+    long long tag;                 // first step of this launch (step tags)
+    int check_prev;                // our previous launch ended at step tag - 1
+    int span;                      // steps this launch publishes (2; the prime 1)
+    unsigned long long timeout_ns;
+    long long interior;            // items before the border runs
+    long long edges;               // border runs (the last items)
+    int flags;                     // TLB_F_POISON_HALOS
+};
+
 struct TbLaunch {
     Fld src, dst;
     long long soffb[Q];    // byte offset of population l's level-0 source from the site
@@ -27,6 +46,7 @@ struct TbLaunch {
     unsigned *ctr;         // zeroed work-item counter
     TlbStatus *st1, *st2;  // status of step s and of step s + 1
     int step;
+    TbPeer pe;             // PEER launches only
 };
 
 }  // namespace tb2
@@ -34,5 +54,8 @@ struct TbLaunch {
 cudaError_t tb2_set_const(const StencilConst &h);
 int tb2_rows(int cfg);     // level-1 rows per strip of configuration cfg
 cudaError_t tb2_launch(const tb2::TbLaunch &T, bool exact, int cfg, int sms, cudaStream_t s);
+// the ring variant (64 x 2, 2 CTAs/SM), and its halo fill
+cudaError_t tb2_launch_peer(const tb2::TbLaunch &T, bool exact, int sms, cudaStream_t s);
+cudaError_t tb2_prime_peer(const tb2::TbLaunch &T, cudaStream_t s);
 
 }  // namespace tlb

@@ -869,9 +869,12 @@ static int tb2_run_length(int Lx, int ns, bool walls, int ctas) {
     return best_run;
 }
 
-int tlb_step2_self(const TlbField *prv, const TlbField *nxt, const TlbParams *p, int walls,
-                   int periodic_y, int count_neg, TlbStatus *status1, TlbStatus *status2,
-                   int step, tlb_stream_t stream) {
+// Launch set-up shared by the one-tile and the ring two-step kernels: checks,
+// offsets, strips and runs (cfg: kernel shape; min_runs: runs per strip at
+// least -- the ring variant needs a first and a last run).
+static int tb2_setup(tb2::TbLaunch &T, const TlbField *prv, const TlbField *nxt,
+                     const TlbParams *p, int flags, TlbStatus *status1, TlbStatus *status2,
+                     int step, int cfg, int min_runs, int &sms) {
     int e;
     if ((e = check_stencil())) return e;
     if ((e = check_params(p))) return e;
@@ -880,17 +883,13 @@ int tlb_step2_self(const TlbField *prv, const TlbField *nxt, const TlbParams *p,
     if (prv->Lx < 8 || prv->Ly < 8)
         return fail(TLB_ERR_UNSUPPORTED, "two-step kernel: tile smaller than 8x8");
     if (prv->base == nxt->base) return fail(TLB_ERR_CONTRACT, "step2: prv and nxt alias");
+    const bool walls = (flags & TLB_F_WALL_BOT) != 0;
     if (walls && (!(p->Twall_top > 0.0) || !(p->Twall_bot > 0.0)))
         return fail(TLB_ERR_DOMAIN, "equilibrium requires rho > 0 and T > 0");
-    tb2::TbLaunch T;
     memset(&T, 0, sizeof T);
     T.src = mkfld(prv);
     T.dst = mkfld(nxt);
     T.P = mkphys(p);
-    int flags = TLB_F_WRAP_X;
-    if (walls) flags |= TLB_F_WALL_BOT | TLB_F_WALL_TOP | TLB_F_CLAMP_Y;
-    else if (periodic_y) flags |= TLB_F_WRAP_Y;
-    if (count_neg) flags |= TLB_F_COUNT_NEG;
     T.flags = flags;
     SiteLaunch W;
     memset(&W, 0, sizeof W);
@@ -904,18 +903,16 @@ int tlb_step2_self(const TlbField *prv, const TlbField *nxt, const TlbParams *p,
     T.st1 = status1;
     T.st2 = status2;
     T.step = step;
-    int dev = 0, sms = 0;
+    int dev = 0;
     TLB_CUDA_CHECK(cudaGetDevice(&dev));
     TLB_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    const int hs = tb2_rows(g_tb2_cfg) - 6;     // output rows per strip, at most
+    const int hs = tb2_rows(cfg) - 6;     // output rows per strip, at most
     T.ns = (prv->Ly + hs - 1) / hs;
     // work items: runs of run_l columns of a strip; wall strips (bc rows)
     // first, in runs of half the length
     const int Lx = prv->Lx;
-    int dev0 = 0, sms0 = 0;
-    TLB_CUDA_CHECK(cudaGetDevice(&dev0));
-    TLB_CUDA_CHECK(cudaDeviceGetAttribute(&sms0, cudaDevAttrMultiProcessorCount, dev0));
-    T.run_l = tb2_run_length(Lx, T.ns, walls != 0, sms0 * (g_tb2_cfg == 1 ? 2 : 1));
+    T.run_l = tb2_run_length(Lx, T.ns, walls, sms * (cfg == 1 ? 2 : 1));
+    if ((Lx + T.run_l - 1) / T.run_l < min_runs) T.run_l = (Lx + min_runs - 1) / min_runs;
     T.run_h = T.run_l / 2 > 8 ? T.run_l / 2 : T.run_l;
     T.nheavy = walls ? (T.ns >= 2 ? 2 : 1) : 0;
     T.first_light = walls ? 1 : 0;
@@ -925,6 +922,20 @@ int tlb_step2_self(const TlbField *prv, const TlbField *nxt, const TlbParams *p,
     T.items = (long long)T.nheavy * T.hruns + (long long)nlight * T.lruns;
     if (!g_tb2_ctr[dev]) return fail(TLB_ERR_STENCIL, "stencil not set on device %d", dev);
     T.ctr = g_tb2_ctr[dev];
+    return TLB_OK;
+}
+
+int tlb_step2_self(const TlbField *prv, const TlbField *nxt, const TlbParams *p, int walls,
+                   int periodic_y, int count_neg, TlbStatus *status1, TlbStatus *status2,
+                   int step, tlb_stream_t stream) {
+    int flags = TLB_F_WRAP_X;
+    if (walls) flags |= TLB_F_WALL_BOT | TLB_F_WALL_TOP | TLB_F_CLAMP_Y;
+    else if (periodic_y) flags |= TLB_F_WRAP_Y;
+    if (count_neg) flags |= TLB_F_COUNT_NEG;
+    tb2::TbLaunch T;
+    int sms = 0;
+    int e = tb2_setup(T, prv, nxt, p, flags, status1, status2, step, g_tb2_cfg, 1, sms);
+    if (e) return e;
     TLB_CUDA_CHECK(cudaMemsetAsync(T.ctr, 0, sizeof(unsigned), (cudaStream_t)stream));
     TLB_CUDA_CHECK(tb2_launch(T, p->arith == TLB_ARITH_EXACT, g_tb2_cfg, sms, (cudaStream_t)stream));
     return TLB_OK;

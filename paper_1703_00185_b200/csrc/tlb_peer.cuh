@@ -26,10 +26,6 @@
 // once instead of waiting again).
 #pragma once
 
-// Default bound of the border blocks' wait; tlb_peer_set_timeout sets it per
-// peer object (the host passes its fabric timeout).
-#define TLB_PEER_TIMEOUT_NS 5000000000ull
-
 // directions d = (dx, dy): 0 left, 1 right, 2 down, 3 up, 4 down-left,
 // 5 down-right, 6 up-left, 7 up-right; POPP(d) is the reverse direction
 __host__ __device__ constexpr int PDX(int d) {
@@ -39,19 +35,6 @@ __host__ __device__ constexpr int PDY(int d) {
     return (d == 2 || d == 4 || d == 5) ? -1 : (d == 3 || d == 6 || d == 7) ? 1 : 0;
 }
 __host__ __device__ constexpr int POPP(int d) { return d < 4 ? (d ^ 1) : 11 - d; }
-
-// mailbox layout (u64): [0..7] value published by the neighbour in direction
-// d, [8] border-block counter, [9] sticky failure flag.  A published value
-// carries the neighbour's step count (bits 0..39), the step tag = its step
-// number + 1 (bits 40..62; runtime.py:151-154's step check) and, in bit 63,
-// "I failed" (a timed-out rank poisons what it publishes, so its neighbours
-// stop too instead of using halos that were never written).
-#define TLB_MB_COUNTER 8
-#define TLB_MB_STICKY 9
-#define TLB_MB_CTR_MASK ((1ull << 40) - 1)
-#define TLB_MB_TAG_SHIFT 40
-#define TLB_MB_TAG_MASK ((1ull << 23) - 1)
-#define TLB_MB_POISON (1ull << 63)
 
 struct TlbPeer {
     int device = 0;
@@ -77,18 +60,6 @@ struct PeerLaunch {
     Rect br[4];                    // left, right (full height), bottom, top (in between)
     unsigned br_end[4];
 };
-
-__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
-    unsigned long long v;
-    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-
-__device__ __forceinline__ unsigned long long globaltimer() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    return t;
-}
 
 // Store the populations of f that cross into direction d: at halo depth
 // (ddx, ddy) those with c_x <= -ddx (left) / >= ddx (right) and c_y <= -ddy
@@ -551,6 +522,77 @@ int tlb_peer_prime(tlb_peer_t pr, const TlbField *prv, int prv_index, const TlbP
     if (e) return e;
     k_peer_step<false, true><<<P.nbb, 128, 0, (cudaStream_t)stream>>>(L, P);
     return launch_check("peer prime");
+}
+
+}  // extern "C"
+
+// ---- two steps per launch on the 1-D ring (tb2.cu, PEER) -----------------
+static int tb2_peer_setup(tlb_peer_t pr, const TlbField *prv, const TlbField *nxt, int buf_index,
+                          const TlbParams *p, int flags, TlbStatus *st1, TlbStatus *st2,
+                          unsigned long long *mailbox, int64_t peer_step, int64_t step,
+                          int check_prev, tb2::TbLaunch &T, int &sms) {
+    if (!pr || !mailbox) return fail(TLB_ERR_CONTRACT, "null peer or mailbox");
+    if (!pr->present[0] || !pr->present[1])
+        return fail(TLB_ERR_CONTRACT, "two-step peer launch: needs left and right neighbours");
+    for (int d = 2; d < 8; ++d)
+        if (pr->present[d])
+            return fail(TLB_ERR_UNSUPPORTED, "two-step peer launch: 1-D X ring only");
+    if (buf_index != 0 && buf_index != 1) return fail(TLB_ERR_CONTRACT, "buffer index must be 0/1");
+    if (prv->Hx < 6) return fail(TLB_ERR_CONTRACT, "two-step peer launch: X halo must be >= 6");
+    if (prv->Lx < 12) return fail(TLB_ERR_UNSUPPORTED, "two-step peer launch: tile narrower than 12");
+    if (flags & TLB_F_WRAP_X) return fail(TLB_ERR_CONTRACT, "peer step: X halos are remote");
+    int e = tb2_setup(T, prv, nxt, p, flags & (TLB_F_WALL_BOT | TLB_F_WALL_TOP | TLB_F_CLAMP_Y |
+                                               TLB_F_WRAP_Y | TLB_F_COUNT_NEG),
+                      st1, st2, (int)step, 1, 2, sms);
+    if (e) return e;
+    for (int d = 0; d < 2; ++d) {
+        T.pe.nb[d] = pr->buf[d][buf_index];
+        T.pe.nbmb[d] = pr->mb[d];
+    }
+    T.pe.mb = mailbox;
+    T.pe.need = peer_step;
+    T.pe.tag = step;
+    T.pe.check_prev = check_prev;
+    T.pe.span = 2;
+    T.pe.timeout_ns = pr->timeout_ns;
+    T.pe.edges = 2LL * T.ns;
+    T.pe.interior = T.items - T.pe.edges;
+    // the work counter lives in this rank's mailbox ([10]): ranks sharing a
+    // GPU run their launches concurrently and must not share it
+    T.ctr = reinterpret_cast<unsigned *>(mailbox + TLB_MB_WORK);
+    return TLB_OK;
+}
+
+extern "C" {
+
+int tlb_peer_step2(tlb_peer_t pr, const TlbField *prv, const TlbField *nxt, int nxt_index,
+                   const TlbParams *p, int flags, TlbStatus *status1, TlbStatus *status2,
+                   unsigned long long *mailbox, int64_t peer_step, int64_t step_tag,
+                   int check_prev, tlb_stream_t stream) {
+    tb2::TbLaunch T;
+    int sms = 0;
+    int e = tb2_peer_setup(pr, prv, nxt, nxt_index, p, flags, status1, status2, mailbox,
+                           peer_step, step_tag, check_prev, T, sms);
+    if (e) return e;
+    TLB_CUDA_CHECK(cudaMemsetAsync(T.ctr, 0, sizeof(unsigned), (cudaStream_t)stream));
+    TLB_CUDA_CHECK(tb2_launch_peer(T, p->arith == TLB_ARITH_EXACT, sms, (cudaStream_t)stream));
+    return TLB_OK;
+}
+
+int tlb_peer_prime2(tlb_peer_t pr, const TlbField *prv, int prv_index, const TlbParams *p,
+                    TlbStatus *status, unsigned long long *mailbox, int64_t peer_step,
+                    int64_t step_tag, tlb_stream_t stream) {
+    tb2::TbLaunch T;
+    int sms = 0;
+    // any second buffer will do for the checks: the prime reads prv only
+    TlbField other = *prv;
+    other.base = prv->base + 1;
+    int e = tb2_peer_setup(pr, prv, &other, prv_index, p, 0, status, status, mailbox, peer_step,
+                           step_tag, 0, T, sms);
+    if (e) return e;
+    T.pe.span = 1;          // published as one step (step_tag)
+    TLB_CUDA_CHECK(tb2_prime_peer(T, (cudaStream_t)stream));
+    return TLB_OK;
 }
 
 }  // extern "C"

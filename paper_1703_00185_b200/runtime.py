@@ -372,7 +372,19 @@ class RankWorker:
         self.debug_poison = debug_poison
         self.device = torch.device(device) if device is not None else torch.device(
             "cuda", torch.cuda.current_device())
-        self.geom = LatticeGeometry(tile.Lx, tile.Ly, halo, halo, vs.Q, layout)
+        # a 1-D ring rank that will pair steps across GPUs (tlb_peer_step2)
+        # needs 6 X halo columns: both steps' pull reach
+        order0 = params.eq_order if params.eq_order is not None else vs.eq_order
+        nb0 = tile.neighbors
+        ring_1d = (nb0["left"] != tile.rank and tile.grid[1] == 1)
+        self.pair_ring_wanted = (
+            ring_1d and schedule == "overlapped" and exchange in ("auto", "p2p")
+            and vs.Q == 37 and order0 == 4 and tile.Lx >= 12 and tile.Ly >= 8
+            and not debug_poison and temporal != "off"
+            and (temporal == "on" or (params.arith == "fast"
+                                      and tile.Lx * tile.Ly >= self.PAIR_MIN_SITES)))
+        hx = max(halo, 6) if self.pair_ring_wanted else halo
+        self.geom = LatticeGeometry(tile.Lx, tile.Ly, hx, halo, vs.Q, layout)
         self.halo = halo
         nb = tile.neighbors
         self.x_self = nb["left"] == tile.rank
@@ -446,7 +458,7 @@ class RankWorker:
         self._retained = []
         self._metrics = []
         self.snapshots = []
-        self._primed = False
+        self._halo_depth = 0    # peer halos filled: 0 no, 3 single-step, 6 pair depth
 
     def _setup_peer(self, fabric, strict=False):
         """Map the ring neighbours' field buffers and mailboxes (CUDA IPC over
@@ -519,7 +531,7 @@ class RankWorker:
         self._bufA = self.prv.data.data_ptr()
         self._peer_step = 0
         self._last_tag = None
-        self._primed = False
+        self._halo_depth = 0
         if self.debug_poison:
             # both buffers' halos start poisoned; afterwards every peer step
             # re-poisons prv's halos once its border blocks have read them
@@ -763,6 +775,10 @@ class RankWorker:
         if self.temporal == "off" or self.schedule != "overlapped" or self.debug_poison:
             return False
         order = self.params.eq_order if self.params.eq_order is not None else self.vs.eq_order
+        if self._peer is not None:
+            # across GPUs on the 1-D ring (tlb_peer_step2): decided with the
+            # halo width at construction
+            return self.pair_ring_wanted and self.geom.Hx >= 6 and not self.y_exchange
         if not (self.x_self and not self.y_exchange and self._ring is None and self._peer is None
                 and (self.y_self or (self.wall_bot and self.wall_top))
                 and self.vs.Q == 37 and order == 4 and self.geom.Lx >= 8 and self.geom.Ly >= 8):
@@ -791,10 +807,33 @@ class RankWorker:
             ev = ("graph", torch.cuda.Event(enable_timing=True),
                   torch.cuda.Event(enable_timing=True), 2)
             ev[1].record(self.stream)
-        self._check(_lib.load().tlb_step2_self(
-            field_desc(self.prv), field_desc(self.nxt), self.tparams, int(self.wall_bot),
-            int(self.y_self), 1, s1.data_ptr(), s2.data_ptr(), int(step_no), self._sp()),
-            "step2")
+        lib = _lib.load()
+        if self._peer is not None:
+            if self._halo_depth < 6:
+                # 6-deep halos: the border columns' populations the
+                # neighbours' level-1 halo sites pull, as if step_no-1 had
+                # just run (counts as a peer step)
+                prv_index = 0 if self.prv.data.data_ptr() == self._bufA else 1
+                self._check(lib.tlb_peer_prime2(
+                    self._peer, field_desc(self.prv), prv_index, self.tparams, s1.data_ptr(),
+                    self.mailbox.data_ptr(), self._peer_step, step_no - 1, self._sp()),
+                    "peer prime2")
+                self._peer_step += 1
+                self._last_tag = step_no - 1
+            nxt_index = 0 if self.nxt.data.data_ptr() == self._bufA else 1
+            self._check(lib.tlb_peer_step2(
+                self._peer, field_desc(self.prv), field_desc(self.nxt), nxt_index,
+                self.tparams, self._flags(), s1.data_ptr(), s2.data_ptr(),
+                self.mailbox.data_ptr(), self._peer_step, step_no,
+                int(self._last_tag == step_no - 1), self._sp()), "peer step2")
+            self._peer_step += 1
+            self._last_tag = step_no + 1
+            self._halo_depth = 6
+        else:
+            self._check(lib.tlb_step2_self(
+                field_desc(self.prv), field_desc(self.nxt), self.tparams, int(self.wall_bot),
+                int(self.y_self), 1, s1.data_ptr(), s2.data_ptr(), int(step_no), self._sp()),
+                "step2")
         if ev is not None:
             ev[2].record(self.stream)
         self._records.append(_StepRecord(step_no, s1, ev))
@@ -921,7 +960,7 @@ class RankWorker:
         flags = self._flags()
         self._flags_now = flags
         if self._peer is not None:
-            if not self._primed:
+            if self._halo_depth < 3:
                 # fill prv's halos once: the border sites push their values
                 # into the neighbours' halos as if step_no-1 had just run;
                 # afterwards every step's border threads write them directly
@@ -932,7 +971,6 @@ class RankWorker:
                     "peer prime")
                 self._peer_step += 1
                 self._last_tag = step_no - 1
-                self._primed = True
             nxt_index = 0 if self.nxt.data.data_ptr() == self._bufA else 1
             pflags = flags | (_lib.F_POISON_HALOS if self.debug_poison else 0)
             self._rec(ev, 1)
@@ -942,6 +980,7 @@ class RankWorker:
                 step_no, int(self._last_tag == step_no - 1), self._sp()), "peer step")
             self._peer_step += 1
             self._last_tag = step_no
+            self._halo_depth = 3      # a single step refills only the face-plan lines
             self._rec(ev, 2)
             self._bulk_timed = True
             return
@@ -1149,7 +1188,7 @@ class RankWorker:
     def load_block(self, block):
         """prv[phys] = block (sim.py:74-75); block is (Q, Lx, Ly)."""
         torch = _lib.torch_cuda()
-        self._primed = False
+        self._halo_depth = 0
         g = self.geom
         self.stream.wait_stream(torch.cuda.current_stream(self.device))
         with torch.cuda.stream(self.stream):

@@ -254,20 +254,32 @@ def run(cfg: SimConfig, f0=None) -> RunResult:
             s += n
             if cfg.snapshot_every and s % cfg.snapshot_every == 0:
                 snapshot(s)
-        for s in range(0 if not single else cfg.steps, cfg.steps):
-            # lock step over the in-process ranks: every rank's sends are
-            # posted before any rank waits (Y faces, then X faces)
-            for phase in ("step_begin", "step_mid", "step_end"):
+        # ranks on a 1-D ring of peers pair steps (tlb_peer_step2) unless a
+        # snapshot falls between the two
+        pair = not single and all(w.pairable() for w in workers)
+        s = 0 if not single else cfg.steps
+        while s < cfg.steps:
+            every = cfg.snapshot_every
+            if pair and s + 1 < cfg.steps and not (every and (s + 1) % every == 0):
                 for w in workers:
                     with torch.cuda.device(w.device):
-                        getattr(w, phase)(s)
+                        w.step_pair(s)
+                s += 2
+            else:
+                # lock step over the in-process ranks: every rank's sends are
+                # posted before any rank waits (Y faces, then X faces)
+                for phase in ("step_begin", "step_mid", "step_end"):
+                    for w in workers:
+                        with torch.cuda.device(w.device):
+                            getattr(w, phase)(s)
+                s += 1
             if cfg.debug_poison:
                 for w in workers:
                     if not bool(torch.isfinite(w.physical_block()).all()):
                         raise ThermoLBError(
-                            f"rank {w.tile.rank}: NaN reached physical cells at step {s}")
-            if cfg.snapshot_every and (s + 1) % cfg.snapshot_every == 0:
-                snapshot(s + 1)
+                            f"rank {w.tile.rank}: NaN reached physical cells at step {s - 1}")
+            if every and s % every == 0:
+                snapshot(s)
         for w in workers:
             w.synchronize()
         wall = time.perf_counter() - t0

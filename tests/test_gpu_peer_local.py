@@ -190,3 +190,102 @@ def test_peer_prime_then_reload(orc):
         w.close()
     want, _ = _oracle(orc, 48, 40, 5, p, False)
     assert np.array_equal(got, want)
+
+
+# ---- two steps per launch across the ring (tlb_peer_step2) ---------------
+
+PAIR_CASES = [
+    # (Np, Lx, Ly, periodic_y, steps, snapshot_every)
+    (2, 2 * 40, 70, False, 8, 0),       # walls, several strips, even steps
+    (2, 2 * 24, 40, True, 9, 0),        # periodic Y, odd: a final single step
+    (4, 4 * 20, 130, False, 11, 3),     # 4 ranks, snapshots between pairs
+    (3, 3 * 12, 24, False, 6, 0),       # the narrowest tile (12 columns)
+]
+
+
+@pytest.mark.parametrize("case", PAIR_CASES, ids=lambda c: "-".join(map(str, c)))
+@pytest.mark.parametrize("arith", ["exact", "fast"])
+def test_peer_pairs_match_oracle(orc, case, arith):
+    """In-process ranks on one GPU with temporal="on": the ring kernel's
+    border runs read 6-column halos their neighbours stored and store their
+    own; bitwise (exact) / 1e-12 (fast) against the oracle, per-step
+    negatives, snapshots taken between pairs."""
+    Np, Lx, Ly, periodic, steps, every = case
+    p = _params(arith)
+    res = tl.run(tl.SimConfig(Lx=Lx, Ly=Ly, Np=Np, tiling="1d", steps=steps, params=p,
+                              init="rayleigh-taylor", exchange="p2p", walls=not periodic,
+                              periodic_y=periodic, devices=(0,), temporal="on",
+                              snapshot_every=every))
+    want, neg = _oracle(orc, Lx, Ly, steps, p, periodic)
+    if arith == "exact":
+        assert np.array_equal(res.populations, want)
+        got = np.zeros(steps, dtype=np.int64)
+        for m in res.metrics:
+            got[m["step"]] += m["negatives"]
+        assert np.array_equal(got, np.asarray(neg)[:steps])
+    else:
+        assert np.max(np.abs(res.populations - want) / np.abs(want)) < 1e-12
+    if every:
+        assert [s for s, _ in res.snapshots] == list(range(every, steps + 1, every))
+
+
+def test_peer_pairs_are_the_kernel_used():
+    """temporal="on" ranks on a 1-D ring allocate 6 halo columns and pair."""
+    vs = _vs()
+    tiles = tl.decompose(48, 40, 2, "1d")
+    fab = tl.Fabric(2)
+    ws = [tl.RankWorker(t, vs, _params(), fab, schedule="overlapped", exchange="p2p",
+                        device=torch.device("cuda", 0), temporal="on") for t in tiles]
+    assert link_local_peers(ws, strict=True)
+    assert all(w.geom.Hx == 6 and w.pairable() for w in ws)
+    for w in ws:
+        w.close()
+
+
+def test_peer_pairs_mixed_with_single_steps(orc):
+    """Pairs, then single steps, then pairs again (the halos are re-primed
+    to 6 columns), then a reload: bitwise equal to the oracle."""
+    vs = _vs()
+    p = _params()
+    tiles = tl.decompose(48, 40, 2, "1d")
+    fab = tl.Fabric(2)
+    ws = [tl.RankWorker(t, vs, p, fab, schedule="overlapped", exchange="p2p",
+                        device=torch.device("cuda", 0), temporal="on") for t in tiles]
+    link_local_peers(ws, strict=True)
+    macro = tl.init.rayleigh_taylor_macro(48, 40, vs)
+    for w in ws:
+        t = w.tile
+        sl = (slice(t.x0, t.x0 + t.Lx), slice(t.y0, t.y0 + t.Ly))
+        w.load_block(tl.equilibrium(*[torch.as_tensor(np.ascontiguousarray(a[sl]),
+                                                      device="cuda") for a in macro], vs))
+    plan = ["pair", "single", "single", "pair", "pair", "single", "pair"]
+    s = 0
+    for kind in plan:
+        for w in ws:
+            (w.step_pair if kind == "pair" else w.step)(s)
+        s += 2 if kind == "pair" else 1
+    got = np.concatenate([w.physical_block().cpu().numpy() for w in ws], axis=1)
+    for w in ws:
+        w.collect()
+        w.close()
+    want, _ = _oracle(orc, 48, 40, s, p, False)
+    assert np.array_equal(got, want)
+
+
+def test_peer_pairs_stalled_neighbour_times_out():
+    """A pair launch whose neighbour never steps: DeadlockError after the
+    fabric timeout, no hang."""
+    vs = _vs()
+    tiles = tl.decompose(48, 40, 2, "1d")
+    fab = tl.Fabric(2, timeout=0.5)
+    ws = [tl.RankWorker(t, vs, _params(), fab, schedule="overlapped", exchange="p2p",
+                        device=torch.device("cuda", 0), temporal="on", timing="off")
+          for t in tiles]
+    link_local_peers(ws, strict=True)
+    for w in ws:
+        w.load_block(torch.full((37, w.tile.Lx, 40), 0.02, dtype=torch.float64))
+    ws[0].step_pair(0)      # primes (waits for rank 1's prime: never comes)
+    with pytest.raises(DeadlockError):
+        ws[0].collect()
+    for w in ws:
+        w.close()
