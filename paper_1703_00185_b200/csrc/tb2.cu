@@ -222,11 +222,17 @@ __device__ __forceinline__ void item_of(const TbLaunch &T, long long i, int &str
     xb += T.src.Hx;
 }
 
-// Ring variant: the same runs, the border runs (first and last of every
-// strip: they read the X halos and store into the neighbours) last.
+// Ring variant: the same runs; the border runs (first and last of every
+// strip: they read the X halos and store into the neighbours) start the
+// second wave -- late enough that the neighbours' previous launch (which
+// ended about when ours did) has published, early enough that their
+// slower coherent loads and remote stores do not form the launch's tail.
 __device__ __forceinline__ void item_of_peer(const TbLaunch &T, long long i, int &strip,
                                              int &xa, int &xb, bool &edge) {
     const int Lx = T.src.Lx;
+    const long long e0 = T.pe.first_edge;
+    if (i >= e0 && i < e0 + T.pe.edges) i = T.pe.interior + (i - e0);   // a border run
+    else if (i >= e0) i -= T.pe.edges;                                     // interior after
     const long long hi = (long long)T.nheavy * (T.hruns - 2);
     const long long li = (long long)(T.ns - T.nheavy) * (T.lruns - 2);
     int rl, r;
@@ -674,7 +680,10 @@ int tb2_rows(int cfg) {
     return (cfg == 1 || cfg == 4) ? 64 : (cfg == 2 || cfg == 6) ? 96 : 128;
 }
 
-cudaError_t tb2_launch_peer(const tb2::TbLaunch &T, bool exact, int sms, cudaStream_t s) {
+cudaError_t tb2_launch_peer(const tb2::TbLaunch &T0, bool exact, int sms, cudaStream_t s) {
+    tb2::TbLaunch T = T0;
+    const long long grid = (long long)sms * 2;      // launch_cfg's grid for 64 x 2, 2/SM
+    T.pe.first_edge = T.pe.interior < grid ? T.pe.interior : grid;
     return exact ? tb2::launch_cfg<true, 64, 2, 2, true>(T, sms, s)
                  : tb2::launch_cfg<false, 64, 2, 2, true>(T, sms, s);
 }

@@ -27,8 +27,9 @@ struct TbPeer {
     int check_prev;                // our previous launch ended at step tag - 1
     int span;                      // steps this launch publishes (2; the prime 1)
     unsigned long long timeout_ns;
-    long long interior;            // items before the border runs
-    long long edges;               // border runs (the last items)
+    long long interior;            // items that are not border runs
+    long long edges;               // border runs
+    long long first_edge;          // item index of the first border run
     int flags;                     // TLB_F_POISON_HALOS
 };
 

@@ -778,7 +778,8 @@ class RankWorker:
         if self._peer is not None:
             # across GPUs on the 1-D ring (tlb_peer_step2): decided with the
             # halo width at construction
-            return self.pair_ring_wanted and self.geom.Hx >= 6 and not self.y_exchange
+            return (self.pair_ring_wanted and self.geom.Hx >= 6 and not self.y_exchange
+                    and (self.temporal == "on" or self.tparams.arith == _lib.ARITH["fast"]))
         if not (self.x_self and not self.y_exchange and self._ring is None and self._peer is None
                 and (self.y_self or (self.wall_bot and self.wall_top))
                 and self.vs.Q == 37 and order == 4 and self.geom.Lx >= 8 and self.geom.Ly >= 8):

@@ -92,6 +92,28 @@ def main():
                       flush=True)
                 ok &= same
             assert len(res.metrics) == steps
+    # two steps per launch across the GPUs (tlb_peer_step2 over CUDA IPC):
+    # walls and periodic Y, an odd step count (a final single step) and
+    # snapshots between pairs
+    for periodic in (False, True):
+        for arith in ("exact", "fast"):
+            pp = tl.PhysicsParams(tau=p.tau, gx=p.gx, gy=p.gy, Twall_top=p.Twall_top,
+                                  Twall_bot=p.Twall_bot, arith=arith)
+            res = tl.run(tl.SimConfig(Lx=Lx, Ly=Ly, Np=world, steps=steps, params=pp,
+                                      init="rayleigh-taylor", exchange="p2p", temporal="on",
+                                      walls=not periodic, periodic_y=periodic,
+                                      snapshot_every=4))
+            if rank == 0:
+                ref = want_periodic if periodic else want
+                if arith == "exact":
+                    same = np.array_equal(res.populations, ref)
+                else:
+                    same = bool(np.max(np.abs(res.populations - ref) / np.abs(ref)) < 1e-12)
+                same &= [s for s, _ in res.snapshots] == [4, 8]
+                print(f"pairs exchange=p2p arith={arith} periodic={periodic} world={world} "
+                      f"ok={same} mlups={res.mlups:.1f}", flush=True)
+                ok &= same
+            assert len(res.metrics) == steps
     dist.barrier()
     if rank == 0:
         print("DIST OK" if ok else "DIST FAIL", flush=True)
