@@ -400,7 +400,10 @@ __global__ void __launch_bounds__(ROWS * LANES, MINB) k_tb2(const __grid_constan
             return PEER ? x : x < Hx ? x + Lx : (x >= Hx + Lx ? x - Lx : x);
         };
         double f[Q];
-        if (row1) gather0<!PEER>(f, T, wrapx(xa - 3 + lane), y1s, edge);
+        // only gathers within 3 columns of a tile edge read the halos the
+        // neighbours store: those (and only those) take the coherent path
+        auto halo_col = [&](int x) { return PEER && edge && (x < Hx + 3 || x >= Hx + Lx - 3); };
+        if (row1) gather0<!PEER>(f, T, wrapx(xa - 3 + lane), y1s, halo_col(xa - 3 + lane));
         // ring slots of level-1 column j (written) and of the columns level 2
         // reads (j - 3 - c), per c_x group; advanced by LANES per iteration
         int ws[7], rs[7];
@@ -422,7 +425,7 @@ __global__ void __launch_bounds__(ROWS * LANES, MINB) k_tb2(const __grid_constan
             }
             // the next level-1 column's HBM gather, in flight during level 2
             if (row1 && k + 1 < K && X1 + LANES < xb + 3)
-                gather0<!PEER>(f, T, wrapx(X1 + LANES), y1s, edge);
+                gather0<!PEER>(f, T, wrapx(X1 + LANES), y1s, halo_col(X1 + LANES));
             __syncthreads();
             const int X2 = X1 - 3;
             if (row2 && X2 >= xa && X2 < xb) {
@@ -508,13 +511,17 @@ __global__ void k_tb2_prime(const __grid_constant__ TbLaunch T) {
 template <bool EXACT, int ROWS, int LANES, int MINB, bool PEER = false>
 static cudaError_t launch_cfg(const TbLaunch &T, int sms, cudaStream_t s) {
     const size_t smem = (size_t)slots(LANES) * ROWS * sizeof(double);
-    static bool attr = false;
+    // the shared-memory opt-in is per device: one process may drive several
+    static bool attr[64] = {};
+    int dev = 0;
+    cudaError_t e0 = cudaGetDevice(&dev);
+    if (e0 != cudaSuccess) return e0;
     auto *fn = k_tb2<EXACT, ROWS, LANES, MINB, PEER>;
-    if (!attr) {
+    if (dev < 0 || dev >= 64 || !attr[dev]) {
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem);
         if (e != cudaSuccess) return e;
-        attr = true;
+        if (dev >= 0 && dev < 64) attr[dev] = true;
     }
     long long grid = (long long)sms * MINB;
     if (grid > T.items) grid = T.items;
@@ -656,13 +663,16 @@ __global__ void __launch_bounds__(ROWS * (PL + CL), MINB) k_tb2ws(const __grid_c
 template <bool EXACT, int ROWS, int PL, int CL, int E, int MINB>
 static cudaError_t launch_ws(const TbLaunch &T, int sms, cudaStream_t s) {
     const size_t smem = (size_t)37 * E * ROWS * sizeof(double);
-    static bool attr = false;
+    static bool attr[64] = {};
+    int dev = 0;
+    cudaError_t e0 = cudaGetDevice(&dev);
+    if (e0 != cudaSuccess) return e0;
     auto *fn = k_tb2ws<EXACT, ROWS, PL, CL, E, MINB>;
-    if (!attr) {
+    if (dev < 0 || dev >= 64 || !attr[dev]) {
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem);
         if (e != cudaSuccess) return e;
-        attr = true;
+        if (dev >= 0 && dev < 64) attr[dev] = true;
     }
     long long grid = (long long)sms * MINB;
     if (grid > T.items) grid = T.items;

@@ -787,6 +787,28 @@ class RankWorker:
         return self.temporal == "on" or (self.tparams.arith == _lib.ARITH["fast"] and
                                          self.geom.Lx * self.geom.Ly >= self.PAIR_MIN_SITES)
 
+    def prime_halos(self, step_no, depth, status=None):
+        """Peer-store exchange: make prv's X halos `depth` deep (3: the face
+        plans, for single steps; 6: for step pairs) before step step_no --
+        the border sites push their values into the neighbours' halos as if
+        step_no-1 had just run (counts as a peer step).  A no-op when the
+        halos already are that deep; step()/step_pair() call it themselves,
+        in-process lock-step drivers call it for every rank first so that
+        no rank's first step waits on a prime launched after it."""
+        if self._peer is None or self._halo_depth >= depth:
+            return
+        lib = _lib.load()
+        if status is None:
+            status = self._status_slot().data_ptr()
+        prv_index = 0 if self.prv.data.data_ptr() == self._bufA else 1
+        fn = lib.tlb_peer_prime2 if depth > 3 else lib.tlb_peer_prime
+        self._check(fn(self._peer, field_desc(self.prv), prv_index, self.tparams, status,
+                       self.mailbox.data_ptr(), self._peer_step, step_no - 1, self._sp()),
+                    "peer prime")
+        self._peer_step += 1
+        self._last_tag = step_no - 1
+        self._halo_depth = max(depth, 3)
+
     def step_pair(self, step_no):
         """Steps step_no and step_no + 1 in ONE launch (tlb_step2_self): the
         intermediate state stays in shared memory.  Bitwise equal to
@@ -810,17 +832,7 @@ class RankWorker:
             ev[1].record(self.stream)
         lib = _lib.load()
         if self._peer is not None:
-            if self._halo_depth < 6:
-                # 6-deep halos: the border columns' populations the
-                # neighbours' level-1 halo sites pull, as if step_no-1 had
-                # just run (counts as a peer step)
-                prv_index = 0 if self.prv.data.data_ptr() == self._bufA else 1
-                self._check(lib.tlb_peer_prime2(
-                    self._peer, field_desc(self.prv), prv_index, self.tparams, s1.data_ptr(),
-                    self.mailbox.data_ptr(), self._peer_step, step_no - 1, self._sp()),
-                    "peer prime2")
-                self._peer_step += 1
-                self._last_tag = step_no - 1
+            self.prime_halos(step_no, 6, s1.data_ptr())
             nxt_index = 0 if self.nxt.data.data_ptr() == self._bufA else 1
             self._check(lib.tlb_peer_step2(
                 self._peer, field_desc(self.prv), field_desc(self.nxt), nxt_index,
@@ -961,17 +973,7 @@ class RankWorker:
         flags = self._flags()
         self._flags_now = flags
         if self._peer is not None:
-            if self._halo_depth < 3:
-                # fill prv's halos once: the border sites push their values
-                # into the neighbours' halos as if step_no-1 had just run;
-                # afterwards every step's border threads write them directly
-                prv_index = 0 if self.prv.data.data_ptr() == self._bufA else 1
-                self._check(lib.tlb_peer_prime(
-                    self._peer, field_desc(self.prv), prv_index, self.tparams, st,
-                    self.mailbox.data_ptr(), self._peer_step, step_no - 1, self._sp()),
-                    "peer prime")
-                self._peer_step += 1
-                self._last_tag = step_no - 1
+            self.prime_halos(step_no, 3, st)
             nxt_index = 0 if self.nxt.data.data_ptr() == self._bufA else 1
             pflags = flags | (_lib.F_POISON_HALOS if self.debug_poison else 0)
             self._rec(ev, 1)

@@ -263,9 +263,15 @@ def run(cfg: SimConfig, f0=None) -> RunResult:
             if pair and s + 1 < cfg.steps and not (every and (s + 1) % every == 0):
                 for w in workers:
                     with torch.cuda.device(w.device):
+                        w.prime_halos(s, 6)
+                for w in workers:
+                    with torch.cuda.device(w.device):
                         w.step_pair(s)
                 s += 2
             else:
+                for w in workers:
+                    with torch.cuda.device(w.device):
+                        w.prime_halos(s, 3)
                 # lock step over the in-process ranks: every rank's sends are
                 # posted before any rank waits (Y faces, then X faces)
                 for phase in ("step_begin", "step_mid", "step_end"):

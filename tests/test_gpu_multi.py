@@ -66,3 +66,20 @@ def test_inprocess_ranks_on_two_gpus(orc):
     f0 = orc.equilibrium(*orc.rayleigh_taylor_macro(64, 32, vs.cs2))
     want, _ = orc.run(f0, 6, orc.params6(0.8, 0.0, -1e-5, 1.0, p.Twall_top, p.Twall_bot))
     assert np.array_equal(res.populations, want)
+
+
+@pytest.mark.parametrize("Np", [2, 4])
+def test_inprocess_ring_pairs_on_two_gpus(orc, Np):
+    """Two steps per launch across GPUs (tlb_peer_step2) with in-process
+    ranks on two devices (Np=4: two ranks per device): bitwise vs the oracle,
+    an odd step count (a final single step) included."""
+    vs = tl.build_velocity_set("D2Q37")
+    orc.set_stencil(vs.c, vs.w, vs.cs2)
+    p = tl.PhysicsParams(tau=0.8, gy=-1e-5, Twall_top=0.9 * vs.cs2, Twall_bot=1.1 * vs.cs2)
+    Lx, Ly, steps = 24 * Np, 70, 9
+    res = tl.run(tl.SimConfig(Lx=Lx, Ly=Ly, Np=Np, steps=steps, params=p,
+                              init="rayleigh-taylor", devices=(0, 1), exchange="p2p",
+                              temporal="on"))
+    f0 = orc.equilibrium(*orc.rayleigh_taylor_macro(Lx, Ly, vs.cs2))
+    want, _ = orc.run(f0, steps, orc.params6(0.8, 0.0, -1e-5, 1.0, p.Twall_top, p.Twall_bot))
+    assert np.array_equal(res.populations, want)
