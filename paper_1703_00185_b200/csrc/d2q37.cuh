@@ -396,26 +396,54 @@ struct FastSite {
     double theta, s, vx, vy, W; // W = omega*rho (relax) or rho (bc)
 };
 
+// Order 4: the shell coefficients below as polynomials in the shell's q,
+// with site-level coefficients (a = theta q - s substituted):
+//   A0/W = (1 - th + th^2) + (1/2 - th) a + a^2/8 = a00 + a01 q + a02 q^2
+//   A1/W = 1 + (a - 4 th)/2                     = b0 + b1 q
+//   A2/W = 1/2 + (a - 6 th)/4                   = g0 + g1 q
+// so a shell costs 4 FMAs instead of ~12 (same polynomial, reassociated).
+struct FastQ {
+    double a00, a01, a02, b0, b1, g0, g1;
+};
+__device__ __forceinline__ FastQ fast_q(const FastSite &e) {
+    const double th = e.theta, s = e.s;
+    const double c0 = fma(th, th - 1.0, 1.0);     // 1 - th + th^2
+    const double c1 = 0.5 - th;
+    FastQ k;
+    k.a00 = fma(0.125 * s, s, fma(-c1, s, c0));   // c0 - c1 s + s^2/8
+    k.a01 = th * fma(-0.25, s, c1);               // th (c1 - s/4)
+    k.a02 = 0.125 * th * th;
+    k.b0 = fma(-0.5, s, fma(-2.0, th, 1.0));      // 1 - 2 th - s/2
+    k.b1 = 0.5 * th;
+    k.g0 = fma(-0.25, s, fma(-1.5, th, 0.5));     // 1/2 - 3/2 th - s/4
+    k.g1 = 0.25 * th;
+    return k;
+}
+
 // Hermite polynomial of kernels.py:99-123 regrouped in powers of p:
 // poly = A0 + A1 p + A2 p^2 + A3 p^3 + A4 p^4 with a = theta*q - s:
 // A0 = 1 + (a-2th)/2 + [a^2/8 - th*a + th^2]_{order 4}, A1 = 1 + [(a-4th)/2]_{>=3},
 // A2 = 1/2 + [(a-6th)/4]_{4}, A3 = [1/6]_{>=3}, A4 = [1/24]_{4}.
 template <int ORDER, int MODE, int sh, class F>
-__device__ __forceinline__ void fast_shell(F &f, const FastSite &e, double omr) {
+__device__ __forceinline__ void fast_shell(F &f, const FastSite &e, const FastQ &k,
+                                           double omr) {
     const double q = C.qsh[sh];
-    const double th = e.theta;
-    const double a = fma(th, q, -e.s);
     const double W = e.W * C.wsh[sh];
-    double A0 = fma(0.5, a - 2.0 * th, 1.0);
-    double A1 = 1.0, A2 = 0.5, A3 = 0.0, A4 = 0.0;
-    if constexpr (ORDER >= 3) {
-        A1 = fma(0.5, a - 4.0 * th, 1.0);
-        A3 = 1.0 / 6.0;
-    }
+    double A0, A1 = 1.0, A2 = 0.5, A3 = 0.0, A4 = 0.0;
     if constexpr (ORDER >= 4) {
-        A0 += fma(0.125 * a, a, th * (th - a));
-        A2 = fma(0.25, a - 6.0 * th, 0.5);
+        A0 = fma(fma(k.a02, q, k.a01), q, k.a00);
+        A1 = fma(k.b1, q, k.b0);
+        A2 = fma(k.g1, q, k.g0);
+        A3 = 1.0 / 6.0;
         A4 = 1.0 / 24.0;
+    } else {
+        const double th = e.theta;
+        const double a = fma(th, q, -e.s);
+        A0 = fma(0.5, a - 2.0 * th, 1.0);
+        if constexpr (ORDER >= 3) {
+            A1 = fma(0.5, a - 4.0 * th, 1.0);
+            A3 = 1.0 / 6.0;
+        }
     }
     A0 *= W; A1 *= W; A2 *= W; A3 *= W; A4 *= W;
     constexpr int s0 = SH_START(sh), n = SH_N(sh);
@@ -450,14 +478,16 @@ __device__ __forceinline__ void fast_shell(F &f, const FastSite &e, double omr) 
 
 template <int ORDER, int MODE, class F>
 __device__ __forceinline__ void fast_all(F &f, const FastSite &e, double omr) {
-    fast_shell<ORDER, MODE, 0, F>(f, e, omr);
-    fast_shell<ORDER, MODE, 1, F>(f, e, omr);
-    fast_shell<ORDER, MODE, 2, F>(f, e, omr);
-    fast_shell<ORDER, MODE, 3, F>(f, e, omr);
-    fast_shell<ORDER, MODE, 4, F>(f, e, omr);
-    fast_shell<ORDER, MODE, 5, F>(f, e, omr);
-    fast_shell<ORDER, MODE, 6, F>(f, e, omr);
-    fast_shell<ORDER, MODE, 7, F>(f, e, omr);
+    FastQ k{};
+    if constexpr (ORDER >= 4) k = fast_q(e);
+    fast_shell<ORDER, MODE, 0, F>(f, e, k, omr);
+    fast_shell<ORDER, MODE, 1, F>(f, e, k, omr);
+    fast_shell<ORDER, MODE, 2, F>(f, e, k, omr);
+    fast_shell<ORDER, MODE, 3, F>(f, e, k, omr);
+    fast_shell<ORDER, MODE, 4, F>(f, e, k, omr);
+    fast_shell<ORDER, MODE, 5, F>(f, e, k, omr);
+    fast_shell<ORDER, MODE, 6, F>(f, e, k, omr);
+    fast_shell<ORDER, MODE, 7, F>(f, e, k, omr);
 }
 
 template <int ORDER, class F>
