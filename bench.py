@@ -78,7 +78,7 @@ def ncu_traffic(kernel, layout="column"):
     for path in paths:
         try:
             with open(path + ".sass") as fh:
-                tags = dict(line.strip().split(" ", 1) for line in fh if " " in line)
+                tags = dict(line.strip().rsplit(" ", 1) for line in fh if " " in line)
             rows = list(csv.reader(open(path)))
         except (OSError, ValueError):
             continue
@@ -503,7 +503,7 @@ def gpu_arm(args, rank, world, local_rank):
                             else "<=1e-12 relative (tests/test_gpu_parity.py)")}
 
     w.timing = "sampled"
-    kname = ("k_tb2<%d, 64, 2, 2>" % (1 if args.arith == "exact" else 0) if pair and world == 1
+    kname = ("k_tb2<%d, 64, 2, 2, 0>" % (1 if args.arith == "exact" else 0) if pair and world == 1
              else "k_tb2<%d, 64, 2, 2, 1>" % (1 if args.arith == "exact" else 0) if pair else
              "k_site<3, %d, 4, 0, 4>" % (1 if args.arith == "exact" else 0) if world == 1 else
              "k_peer_step<%d, 0>" % (1 if args.arith == "exact" else 0))

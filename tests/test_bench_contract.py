@@ -27,3 +27,19 @@ def test_reference_arm_json_line():
     assert "workload" in d["config"]
     with open(os.path.join(ROOT, "BASELINE.json")) as fh:
         assert d["metric"] == json.load(fh)["metric"]
+
+
+def test_ncu_traffic_reads_the_sidecar_of_a_capture(monkeypatch):
+    """bench.ncu_traffic trusts a committed ncu capture only for the SASS hash
+    its .sass sidecar records; kernel names contain spaces ("k_tb2<0, 64, 2,
+    2, 0> <hash>"), so the hash is the last field."""
+    import glob
+    import bench
+    sidecars = sorted(glob.glob(os.path.join(ROOT, "profiles", "*ncu*_column_raw*.csv.sass")))
+    assert sidecars
+    with open(sidecars[-1]) as fh:
+        name, h = fh.readline().strip().rsplit(" ", 1)
+    monkeypatch.setattr(bench, "sass_hash", lambda k: h if k == name else "0" * 16)
+    traffic, src = bench.ncu_traffic(name)
+    assert traffic is not None and traffic > 0, src
+    assert bench.ncu_traffic("k_site<9, 9, 9, 9, 9>")[0] is None

@@ -25,8 +25,9 @@ def main():
     a = ap.parse_args()
     if a.hash_only:
         import bench
-        kernels = ["k_tb2<0, 64, 2, 2>", "k_tb2<1, 64, 2, 2>", "k_site<3, 0, 4, 0, 4>",
-                   "k_site<3, 1, 4, 0, 4>"]
+        kernels = ["k_tb2<0, 64, 2, 2, 0>", "k_tb2<1, 64, 2, 2, 0>", "k_tb2<0, 64, 2, 2, 1>",
+                   "k_tb2<1, 64, 2, 2, 1>", "k_site<3, 0, 4, 0, 4>", "k_site<3, 1, 4, 0, 4>",
+                   "k_peer_step<0, 0>", "k_peer_step<1, 0>"]
         with open(a.hash_only + ".sass", "w") as fh:
             for k in kernels:
                 fh.write(f"{k} {bench.sass_hash(k)}\n")
