@@ -57,6 +57,8 @@ class TlbStatus(ctypes.Structure):
 
 
 STATUS_BYTES = ctypes.sizeof(TlbStatus)
+STATUS_FLAGS_OFF = TlbStatus.flags.offset
+STATUS_NEG_OFF = TlbStatus.negatives.offset
 
 _P = ctypes.c_void_p
 _FP = ctypes.POINTER(TlbField)

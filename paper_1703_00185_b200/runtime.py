@@ -1117,25 +1117,30 @@ class RankWorker:
         self.synchronize()
         n = len(self._records)
         raw = self._status_ring[:n].cpu().numpy()
+        # the status blocks as one structured array (flags, negatives):
+        # per-step ctypes copies cost more than the small-tile steps
+        flags = raw[:, _lib.STATUS_FLAGS_OFF:_lib.STATUS_FLAGS_OFF + 4].copy().view(np.uint32)[:, 0]
+        negs = raw[:, _lib.STATUS_NEG_OFF:_lib.STATUS_NEG_OFF + 8].copy().view(np.uint64)[:, 0]
+        bad = np.flatnonzero(flags)
         err = None
-        for rec, row in zip(self._records, raw):
-            s = _lib.TlbStatus.from_buffer_copy(row.tobytes())
+        if len(bad):
+            i = int(bad[0])
+            err = (self._records[i].step, _lib.TlbStatus.from_buffer_copy(raw[i].tobytes()))
+        span = {}          # one elapsed_time per launch (block), not per step
+        nan = float("nan")
+        for rec, neg in zip(self._records, negs.tolist()):
             if rec.events is None:
-                nan = float("nan")
-                m = {"t_comm_nc": nan, "t_comm_c": nan, "t_bulk": nan, "t_border": nan}
-                m["negatives"] = int(s.negatives)
-                self._metrics.append(m)
-                if err is None and s.flags:
-                    err = (rec.step, s)
+                self._metrics.append({"t_comm_nc": nan, "t_comm_c": nan, "t_bulk": nan,
+                                      "t_border": nan, "negatives": neg})
                 continue
             if rec.events[0] == "graph":
-                _, g0, g1, nsteps = rec.events
-                m = {"t_comm_nc": 0.0, "t_comm_c": 0.0,
-                     "t_bulk": g0.elapsed_time(g1) * 1e-3 / nsteps, "t_border": 0.0}
-                m["negatives"] = int(s.negatives)
-                self._metrics.append(m)
-                if err is None and s.flags:
-                    err = (rec.step, s)
+                key = id(rec.events)
+                t = span.get(key)
+                if t is None:
+                    _, g0, g1, nsteps = rec.events
+                    t = span[key] = g0.elapsed_time(g1) * 1e-3 / nsteps
+                self._metrics.append({"t_comm_nc": 0.0, "t_comm_c": 0.0, "t_bulk": t,
+                                      "t_border": 0.0, "negatives": neg})
                 continue
             t0, t1, t2, t3 = rec.events
             if self.schedule == "staged":
@@ -1145,10 +1150,8 @@ class RankWorker:
                 m = {"t_comm_nc": 0.0, "t_comm_c": t0.elapsed_time(t1) * 1e-3,
                      "t_bulk": t1.elapsed_time(t2) * 1e-3,
                      "t_border": t2.elapsed_time(t3) * 1e-3}
-            m["negatives"] = int(s.negatives)
+            m["negatives"] = neg
             self._metrics.append(m)
-            if err is None and s.flags:
-                err = (rec.step, s)
         self._records = []
         self._retained = []
         with _lib.torch_cuda().cuda.stream(self.stream):
