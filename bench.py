@@ -573,10 +573,11 @@ def gpu_arm(args, rank, world, local_rank):
                                  "reports TDP-based uJ/site)"}
                        if clocks and clocks.get("power_w_median") else None),
             "host_enqueue_ms_per_step": round(host_ms, 4),
-            # our kernels per step: the fused step (N=1, or p2p: halo stores
-            # fused in); NCCL ring: pack, bulk, unpack, border (+ NCCL's own)
-            "gpu_launches": (launches if world == 1 else
-                             args.steps * (1 if w.exchange_mode == "p2p" else 4)),
+            # our kernels in the region, per rank: one per step pair (or
+            # step) -- the p2p halo stores are fused in; the NCCL ring adds
+            # pack, unpack and the border launch per step (+ NCCL's own)
+            "gpu_launches": (launches if world == 1 or w.exchange_mode == "p2p" else
+                             args.steps * 4),
         }
         if split:
             out["split"] = split

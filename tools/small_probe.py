@@ -4,7 +4,6 @@ policies, CUDA events around 32-step blocks after a warm-up.
     python tools/small_probe.py [--sizes 256x128,512x256] [--reps 20]
 
 site_graph  : single-step fused kernel k_site, 32 launches in a CUDA graph
-              (programmatic dependent launch; site_graph_nopdl: ordinary)
 pairs_graph : the two-step kernel, 16 launches in a CUDA graph
 (the persistent multi-step, split-site and loop-rolled kernels measured in
 round 2 live on the exp/small-tiles branch; profiles/r02_small.md)
@@ -69,18 +68,9 @@ def main():
                 torch.cuda.synchronize()
                 return gr.replay
 
-            def site_step_nopdl(k):
-                _lib.check(lib.tlb_set_tuning(7, 0), "tune")
-                site_step(k)
-                _lib.check(lib.tlb_set_tuning(7, 1), "tune")
-
             policies = {
                 "site_graph": graph_of(site_step, 1),
-                "site_graph_nopdl": graph_of(site_step_nopdl, 1),
-                "split_graph": graph_of(steps(1, 1), 1),
                 "pairs_graph": graph_of(pair, 2),
-                "split_multi": lambda: steps(1, K)(0),
-                "site_multi": lambda: steps(0, K)(0),
             }
             for name, fn in policies.items():
                 for _ in range(3):
