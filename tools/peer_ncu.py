@@ -20,11 +20,14 @@ import paper_1703_00185_b200 as tl  # noqa: E402
 def main():
     arith = sys.argv[1] if len(sys.argv) > 1 else "fast"
     temporal = sys.argv[2] if len(sys.argv) > 2 else "off"    # "on": tlb_peer_step2
+    # "0": both ranks on GPU 0 (kernel replay works: a rank's launch waits
+    # only on the other rank's previous launch, already done when serialised)
+    devices = tuple(int(d) for d in (sys.argv[3] if len(sys.argv) > 3 else "0,1").split(","))
     vs = tl.build_velocity_set("D2Q37")
     p = tl.PhysicsParams(tau=0.8, gy=-1e-5, Twall_top=0.9 * vs.cs2, Twall_bot=1.1 * vs.cs2,
                          arith=arith)
     res = tl.run(tl.SimConfig(Lx=3840, Ly=2048, Np=2, steps=4, params=p,
-                              init="rayleigh-taylor", devices=(0, 1), exchange="p2p",
+                              init="rayleigh-taylor", devices=devices, exchange="p2p",
                               output="device", recv_timeout=60.0, temporal=temporal))
     print("peer_ncu done", res.mlups, flush=True)
 
