@@ -114,6 +114,15 @@ def main():
                       f"ok={same} mlups={res.mlups:.1f}", flush=True)
                 ok &= same
             assert len(res.metrics) == steps
+    # 6-wide halos (what a ring rank that pairs steps allocates) on the NCCL
+    # ring and the single-step peer kernel: the halo width is a parameter
+    for exchange in ("nccl", "p2p"):
+        res = tl.run(tl.SimConfig(Lx=Lx, Ly=Ly, Np=world, steps=steps, params=p,
+                                  init="rayleigh-taylor", exchange=exchange, halo=6))
+        if rank == 0:
+            same = np.array_equal(res.populations, want)
+            print(f"halo=6 exchange={exchange} world={world} ok={same}", flush=True)
+            ok &= same
     dist.barrier()
     if rank == 0:
         print("DIST OK" if ok else "DIST FAIL", flush=True)

@@ -289,3 +289,16 @@ def test_peer_pairs_stalled_neighbour_times_out():
         ws[0].collect()
     for w in ws:
         w.close()
+
+
+@pytest.mark.parametrize("exchange", ["p2p", "auto"])
+def test_six_wide_halos(orc, exchange):
+    """The halo width is a parameter: 6-wide halos (what a ring rank that
+    pairs steps allocates) with single steps through the peer kernel and
+    through the in-process Fabric exchange: bitwise vs the oracle."""
+    p = _params()
+    res = tl.run(tl.SimConfig(Lx=48, Ly=40, Np=2, tiling="1d", steps=7, params=p,
+                              init="rayleigh-taylor", exchange=exchange, devices=(0,),
+                              halo=6, temporal="off"))
+    want, _ = _oracle(orc, 48, 40, 7, p, False)
+    assert np.array_equal(res.populations, want)
