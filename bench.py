@@ -259,6 +259,37 @@ def numpy_reference_rates(budget_s=60.0):
         out[name] = {"lattice": f"{Lx}x{Ly}", "Np": Np, "cores": Np, "steps": steps,
                      "wall_s": round(res.wall_seconds, 3), "mlups": round(res.mlups, 4),
                      "gflops_fp64": round(res.mlups * FLOP_SITE / 1e3, 3)}
+    # the reference's kernels one by one on one core (SURVEY §8d "per-kernel
+    # split on C2"): propagate and bc over the whole C2 tile, collide on a
+    # 240-column band of it (the same per-site work; ~1/8 of the ~21 s a
+    # full C2 collide takes) scaled to the tile
+    if time.time() - t_start < budget_s:
+        try:
+            from thermolb import allocate_field, bc, collide, propagate
+            from thermolb.geometry import LatticeGeometry
+            from thermolb.init import build_initial_state
+            g = LatticeGeometry(TILE_LX, TILE_LY, 3, 3, vs.Q)
+            prv, nxt = allocate_field(g, vs)
+            prv.pops[:, g.phys_x, g.phys_y] = build_initial_state("rayleigh-taylor", TILE_LX,
+                                                                   TILE_LY, vs)
+            sites = TILE_LX * TILE_LY
+            t0 = time.perf_counter()
+            propagate(prv, nxt, vs)
+            t_prop = time.perf_counter() - t0
+            t0 = time.perf_counter()
+            bc(nxt, p, vs)
+            t_bc = time.perf_counter() - t0
+            band = nxt.pops[:, g.Hx:g.Hx + 240, g.phys_y]
+            t0 = time.perf_counter()
+            collide(band, p, vs)
+            t_col = (time.perf_counter() - t0) * TILE_LX / 240
+            out["split_C2_1core"] = {
+                "propagate_s": round(t_prop, 4), "bc_s": round(t_bc, 4),
+                "collide_s": round(t_col, 3), "collide_sample": "240x2048 band, scaled x8",
+                "propagate_GBps": round(BYTES_SITE * sites / t_prop / 1e9, 3),
+                "collide_gflops": round(FLOP_SITE * sites / t_col / 1e9, 3)}
+        except Exception as e:  # noqa: BLE001 -- report, do not fail the arm
+            out["split_C2_1core"] = {"unavailable": repr(e)[:200]}
     return out
 
 
