@@ -380,6 +380,7 @@ __global__ void __launch_bounds__(ROWS * LANES, MINB) k_tb2(const __grid_constan
             // a neighbour is gone: no compute, but count the run so the
             // (poisoned) publication still happens
             if (threadIdx.x == 0) tb2_peer_done(T.pe, T.pe.edges, T.step + 2);
+            __syncthreads();     // every thread has read s_item before it is reused
             continue;
         }
         const int ys = Hy + (int)((long long)Ly * strip / T.ns);
