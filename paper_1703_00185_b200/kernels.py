@@ -110,14 +110,16 @@ def _raise_status(st, what):
 
 
 def _check_region(geom: LatticeGeometry, region):
-    """kernels.py:149-156."""
-    xs, ys = region
-    xs = slice(*xs.indices(geom.NX))
-    ys = slice(*ys.indices(geom.NY))
-    px, py = geom.phys_x, geom.phys_y
-    if xs.start < px.start or xs.stop > px.stop or ys.start < py.start or ys.stop > py.stop:
-        raise ContractViolation(f"region {region} extends into the halo")
-    return xs, ys
+    """Normalise a (slice_x, slice_y) region in padded coordinates and insist
+    it lies inside the physical sites (kernels.py:149-156: ContractViolation
+    otherwise)."""
+    bounds = []
+    for sl, n, phys in ((region[0], geom.NX, geom.phys_x), (region[1], geom.NY, geom.phys_y)):
+        lo, hi, step = sl.indices(n)
+        if lo < phys.start or hi > phys.stop:
+            raise ContractViolation(f"region {region} extends into the halo")
+        bounds.append(slice(lo, hi, step))
+    return tuple(bounds)
 
 
 def field_desc(f: PopulationField):

@@ -24,6 +24,7 @@ Both decompositions of the reference are supported: the 1-D X ring (the
 north star) and the 2-D grid (Y chain with walls or Y ring).
 """
 
+import collections
 import queue
 import threading
 import time
@@ -65,100 +66,98 @@ def _divisor_hint(L, axis):
 
 
 def decompose(Lx, Ly, Np, tiling, periodic_y=False):
-    """Split the lattice into Np uniform tiles (runtime.py:54-91)."""
-    if tiling == "1d":
-        nx, ny = Np, 1
-    else:
-        nx, ny = tiling
+    """Uniform tiles of an (Lx, Ly) lattice on an nx x ny rank grid, ranks
+    numbered row-major (x fastest); "1d" is the X ring (nx = Np).  Same
+    tiles, neighbour table and errors as the reference (runtime.py:54-91):
+    X always wraps; Y wraps only with periodic_y, else the bottom / top row
+    of ranks owns the walls."""
+    nx, ny = (Np, 1) if tiling == "1d" else tuple(tiling)
     if nx * ny != Np:
         raise ConfigurationError(f"grid {nx}x{ny} does not match Np={Np}")
-    if Lx % nx:
-        raise ConfigurationError(f"Lx={Lx} not divisible by nx={nx}; " + _divisor_hint(Lx, "X"))
-    if Ly % ny:
-        raise ConfigurationError(f"Ly={Ly} not divisible by ny={ny}; " + _divisor_hint(Ly, "Y"))
+    for L, n, ax in ((Lx, nx, "X"), (Ly, ny, "Y")):
+        if L % n:
+            name = "Lx" if ax == "X" else "Ly"
+            raise ConfigurationError(f"{name}={L} not divisible by n{ax.lower()}={n}; "
+                                     + _divisor_hint(L, ax))
     tx, ty = Lx // nx, Ly // ny
-    tiles = []
-    for iy in range(ny):
-        for ix in range(nx):
-            rank = iy * nx + ix
-            left = iy * nx + (ix - 1) % nx
-            right = iy * nx + (ix + 1) % nx
-            if periodic_y:
-                up = ((iy + 1) % ny) * nx + ix
-                down = ((iy - 1) % ny) * nx + ix
-            else:
-                up = (iy + 1) * nx + ix if iy + 1 < ny else None
-                down = (iy - 1) * nx + ix if iy > 0 else None
-            tiles.append(TileAssignment(
-                rank=rank, grid=(nx, ny), coords=(ix, iy), Lx=tx, Ly=ty,
-                x0=ix * tx, y0=iy * ty,
-                neighbors={"left": left, "right": right, "up": up, "down": down},
-                uppermost=(not periodic_y) and iy == ny - 1,
-                lowermost=(not periodic_y) and iy == 0))
-    return tiles
+
+    def rank_of(ix, iy):
+        return (iy % ny) * nx + ix % nx
+
+    def tile(ix, iy):
+        top, bottom = iy == ny - 1, iy == 0
+        if periodic_y:
+            up, down = rank_of(ix, iy + 1), rank_of(ix, iy - 1)
+        else:
+            up = None if top else rank_of(ix, iy + 1)
+            down = None if bottom else rank_of(ix, iy - 1)
+        return TileAssignment(
+            rank=rank_of(ix, iy), grid=(nx, ny), coords=(ix, iy), Lx=tx, Ly=ty,
+            x0=ix * tx, y0=iy * ty,
+            neighbors={"left": rank_of(ix - 1, iy), "right": rank_of(ix + 1, iy),
+                       "up": up, "down": down},
+            uppermost=top and not periodic_y, lowermost=bottom and not periodic_y)
+
+    return [tile(ix, iy) for iy in range(ny) for ix in range(nx)]
 
 
 def face_plans(vs: VelocitySet, depth=DEFAULT_HALO):
-    """plans[(axis, sign)][d-1] = indices l with sign * c_l[axis] >= d
-    (runtime.py:94-107)."""
-    plans = {}
-    for axis in (0, 1):
-        for sign in (1, -1):
-            plans[(axis, sign)] = [np.nonzero(sign * vs.c[:, axis] >= d)[0]
-                                   for d in range(1, depth + 1)]
-    return plans
+    """For each face (axis, sign) and halo depth d = 1..depth, the
+    populations that cross it that far: sign * c_l[axis] >= d
+    (runtime.py:94-107).  plans[(axis, sign)][d - 1] -> index array."""
+    c = np.asarray(vs.c)
+    return {(axis, sign): [np.flatnonzero(sign * c[:, axis] >= d) for d in range(1, depth + 1)]
+            for axis in (0, 1) for sign in (1, -1)}
 
 
 def boundary_bytes_per_site(vs: VelocitySet, depth=DEFAULT_HALO):
-    """Bytes crossing one face per boundary site (runtime.py:110-113)."""
-    return 8 * sum(len(ls) for ls in face_plans(vs, depth)[(0, 1)])
+    """The model's S (runtime.py:110-113): float64 values one boundary site
+    sends across a face, over all depths."""
+    return 8 * int(sum(ls.size for ls in face_plans(vs, depth)[(0, 1)]))
 
 
 # --------------------------------------------------------------- fabrics --
 
 class Fabric:
     """In-process point-to-point channels with the reference's semantics
-    (runtime.py:116-160): ordered, tagged with the step, recv times out with
-    DeadlockError naming the stalled rank, a step mismatch is a
-    ProtocolError.  Payloads are device tensors; the sender attaches a CUDA
-    event so the receiver's stream waits for the pack without a host sync."""
+    (runtime.py:116-160): FIFO per (src, dst, tag), every message carries its
+    step; recv gives up after `timeout` seconds with DeadlockError naming the
+    waiting rank, a message from another step is a ProtocolError, and one
+    rank's failure (fail) makes every waiting recv abort.  Payloads are
+    device tensors; the sender may attach a CUDA event so the receiver's
+    stream waits for the pack without a host sync."""
 
     def __init__(self, Np, timeout=60.0):
-        self.Np = Np
-        self.timeout = timeout
-        self.channels = {}
+        self.Np, self.timeout = Np, timeout
+        self.channels = collections.defaultdict(queue.Queue)
         self.abort = threading.Event()
         self.failures = []
         self._lock = threading.Lock()
 
     def _chan(self, src, dst, tag):
-        key = (src, dst, tag)
-        with self._lock:
-            if key not in self.channels:
-                self.channels[key] = queue.Queue()
-            return self.channels[key]
+        with self._lock:                     # defaultdict insertion is not atomic
+            return self.channels[(src, dst, tag)]
 
     def send(self, src, dst, tag, step, payload, event=None):
         self._chan(src, dst, tag).put((step, payload, event))
 
     def recv(self, dst, src, tag, step, with_event=False):
         chan = self._chan(src, dst, tag)
-        deadline = time.monotonic() + self.timeout
-        while True:
+        give_up = time.monotonic() + self.timeout
+        msg = None
+        while msg is None:
             if self.abort.is_set():
                 raise ThermoLBError(f"rank {dst}: aborted by peer failure")
             try:
-                got_step, payload, event = chan.get(timeout=min(_POLL, self.timeout))
+                msg = chan.get(timeout=min(_POLL, self.timeout))
             except queue.Empty:
-                if time.monotonic() > deadline:
-                    raise DeadlockError(
-                        f"rank {dst} stalled waiting for rank {src} (tag {tag}, step {step})",
-                        rank=dst)
-                continue
-            if got_step != step:
-                raise ProtocolError(
-                    f"rank {dst}: expected step {step} from {src}/{tag}, got {got_step}")
-            return (payload, event) if with_event else payload
+                if time.monotonic() > give_up:
+                    raise DeadlockError(f"rank {dst} stalled waiting for rank {src} "
+                                        f"(tag {tag}, step {step})", rank=dst)
+        got, payload, event = msg
+        if got != step:
+            raise ProtocolError(f"rank {dst}: expected step {step} from {src}/{tag}, got {got}")
+        return (payload, event) if with_event else payload
 
     def fail(self, rank, exc):
         with self._lock:
