@@ -584,6 +584,13 @@ def gpu_arm(args, rank, world, local_rank):
                          "steps_per_launch": steps_per_launch,
                          "bytes_per_site": BYTES_SITE,
                          "bytes_per_site_update": BYTES_SITE // steps_per_launch,
+                         # the rate as the bandwidth a one-step kernel would need
+                         # (592 B per site update): > peak means past the
+                         # single-step HBM roofline
+                         "single_step_equivalent_GBps": round(
+                             achieved * steps_per_launch, 1),
+                         "single_step_equivalent_frac": round(
+                             achieved * steps_per_launch / hbm_peak, 4),
                          "sites_per_launch": kern_sites,
                          "avg_launch_ms": round(kern_ms, 5), "peak_source": peak_src,
                          "launch_timing": ("CUDA events around the K timed steps / launches "
