@@ -1,10 +1,13 @@
-// tb2.cu -- two time steps per launch (temporal blocking) for a tile that is
-// its own X neighbour (one rank: Np = 1, the BASELINE configs[1] step).
+// tb2.cu -- two time steps per launch (temporal blocking): for a tile that
+// is its own X neighbour (one rank: the BASELINE configs[1] step) and, with
+// PEER, for a rank of the 1-D X ring of GPUs (configs[2]/[3]: 6-column X
+// halos, border runs exchanging over NVLink -- see item_of_peer below).
 //
 // The single-step fused kernel moves the algorithmic minimum of ONE step
 // (592 B/site) at the HBM roofline; the only way past it is to stop writing
 // the intermediate state to HBM.  Here each CTA owns a strip of at most
-// HS = 122 output rows and marches along X over a run of columns:
+// ROWS - 6 output rows (58 in the default 64 x 2 shape) and marches along X
+// over a run of columns:
 //
 //   level 1 (step s):   a column of ROWS = HS + 6 sites (the strip plus 3
 //                       rows of halo each side) is gathered from the level-0
