@@ -83,3 +83,19 @@ def test_inprocess_ring_pairs_on_two_gpus(orc, Np):
     f0 = orc.equilibrium(*orc.rayleigh_taylor_macro(Lx, Ly, vs.cs2))
     want, _ = orc.run(f0, steps, orc.params6(0.8, 0.0, -1e-5, 1.0, p.Twall_top, p.Twall_bot))
     assert np.array_equal(res.populations, want)
+
+
+@pytest.mark.parametrize("n", [2, 4])
+def test_torchrun_bench_config_pairs(n):
+    """configs[2] at N = 2 / 4 (1920x2048 per GPU) under torchrun: exact pairs
+    through the ring two-step kernel == exact single steps bitwise; the fast
+    headline path within the 1e-12 contract (tests/dist_fullsize.py)."""
+    if torch.cuda.device_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={n}", "--master-addr", "127.0.0.1",
+           "--master-port", str(_port()), os.path.join(ROOT, "tests", "dist_fullsize.py")]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    print(out.stdout[-3000:], out.stderr[-3000:])
+    assert out.returncode == 0
+    assert "FULLSIZE OK" in out.stdout
