@@ -362,6 +362,8 @@ def gpu_arm(args, rank, world, local_rank):
         Lx, Ly = Lx_tile * grid[0], Ly_tile * grid[1]
     p = tl.PhysicsParams(tau=0.8, gx=0.0, gy=-1e-5, Twall_top=0.9 * vs.cs2,
                          Twall_bot=1.1 * vs.cs2, arith=args.arith)
+    if args.tb2_order != -1:
+        _lib.check(_lib.load().tlb_set_tuning(4, args.tb2_order), "tb2 order")
     tiles = tl.decompose(Lx, Ly, world, "1d" if grid[1] == 1 else grid)
     tile = tiles[rank]
     fabric = tl.DistFabric() if world > 1 else tl.Fabric(1)
@@ -853,6 +855,8 @@ def main():
                          "into the step kernel")
     ap.add_argument("--Lx", type=int, default=TILE_LX, help="tile Lx per GPU")
     ap.add_argument("--Ly", type=int, default=TILE_LY)
+    ap.add_argument("--tb2-order", type=int, default=-1,
+                    help="two-step kernel work order (TLB_TUNE_TB2_ORDER: -1 auto, 0, 1)")
     ap.add_argument("--tiling", default="1d",
                     help="'1d' (north star) or a rank grid 'NXxNY', e.g. 2x2 (paper's 2-D tiling)")
     ap.add_argument("--strong", action="store_true",

@@ -216,8 +216,17 @@ __device__ __forceinline__ void item_of(const TbLaunch &T, long long i, int &str
         xb = xa + T.run_h < Lx ? xa + T.run_h : Lx;
     } else {
         i -= nh;
-        strip = T.first_light + (int)(i / T.lruns);
-        const int r = (int)(i % T.lruns);
+        int r;
+        if (T.runmajor) {
+            // concurrent CTAs share one X range of every strip: the address
+            // span in flight stays ~run columns wide on huge tiles
+            const int nl = T.ns - T.nheavy;
+            strip = T.first_light + (int)(i % nl);
+            r = (int)(i / nl);
+        } else {
+            strip = T.first_light + (int)(i / T.lruns);
+            r = (int)(i % T.lruns);
+        }
         xa = r * T.run_l;
         xb = xa + T.run_l < Lx ? xa + T.run_l : Lx;
     }
@@ -247,8 +256,14 @@ __device__ __forceinline__ void item_of_peer(const TbLaunch &T, long long i, int
         rl = T.run_h;
     } else if (i < hi + li) {
         i -= hi;
-        strip = T.first_light + (int)(i / (T.lruns - 2));
-        r = 1 + (int)(i % (T.lruns - 2));
+        if (T.runmajor) {
+            const int nl = T.ns - T.nheavy;
+            strip = T.first_light + (int)(i % nl);
+            r = 1 + (int)(i / nl);
+        } else {
+            strip = T.first_light + (int)(i / (T.lruns - 2));
+            r = 1 + (int)(i % (T.lruns - 2));
+        }
         rl = T.run_l;
     } else {
         const long long j = i - hi - li;

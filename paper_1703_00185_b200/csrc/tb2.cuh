@@ -43,6 +43,7 @@ struct TbLaunch {
     int ns;                // strips
     int nheavy, hruns, run_h;   // wall strips (first: strip 0, then ns-1), runs each, run length
     int first_light, lruns, run_l;
+    int runmajor;          // light runs enumerated run-major (all strips at one X first)
     long long items;       // nheavy * hruns + light strips * lruns
     unsigned *ctr;         // zeroed work-item counter
     TlbStatus *st1, *st2;  // status of step s and of step s + 1

@@ -56,6 +56,7 @@ static int g_minb = 4;    // tuning: __launch_bounds__ min blocks of the fused k
 // profiles/r02_tb2.md); work-item length: tb2_run_length
 static int g_tb2_cfg = 1;
 static int g_tb2_run = 0;        // two-step kernel: columns per work item (0: auto)
+static int g_tb2_order = -1;     // two-step kernel work order: -1 auto, 0 strip-, 1 run-major
 static unsigned *g_tb2_ctr[64];  // two-step work-item counters (one u32 per device)
 
 // A launch covers an interior rectangle (plain gather: no halo remapping,
@@ -605,6 +606,11 @@ int tlb_set_tuning(int key, int value) {
         g_tb2_run = value;
         return TLB_OK;
     }
+    if (key == TLB_TUNE_TB2_ORDER) {
+        if (value < -1 || value > 1) return fail(TLB_ERR_CONTRACT, "work order must be -1, 0 or 1");
+        g_tb2_order = value;
+        return TLB_OK;
+    }
     if (key == TLB_TUNE_MINBLOCKS) {
         if (value != 1 && value != 4 && value != 5)
             return fail(TLB_ERR_CONTRACT, "min blocks must be 1, 4 or 5");
@@ -619,6 +625,7 @@ int tlb_get_tuning(int key, int *value) {
     if (key == TLB_TUNE_TB2_CFG) *value = g_tb2_cfg;
     else if (key == TLB_TUNE_TB2_RUN) *value = g_tb2_run;
     else if (key == TLB_TUNE_MINBLOCKS) *value = g_minb;
+    else if (key == TLB_TUNE_TB2_ORDER) *value = g_tb2_order;
     else return fail(TLB_ERR_CONTRACT, "unknown tuning key %d", key);
     return TLB_OK;
 }
@@ -920,6 +927,11 @@ static int tb2_setup(tb2::TbLaunch &T, const TlbField *prv, const TlbField *nxt,
     T.hruns = (Lx + T.run_h - 1) / T.run_h;
     T.lruns = (Lx + T.run_l - 1) / T.run_l;
     T.items = (long long)T.nheavy * T.hruns + (long long)nlight * T.lruns;
+    // work order: run-major on huge tiles, where strip-major puts the ~300
+    // concurrent runs all over a tens-of-GB buffer (address translation:
+    // 8192x16384 +18 %; C2 +1 %, C5 -1 %; profiles/r02_tb2.md)
+    const double field_bytes = 8.0 * Q * (double)(prv->Lx + 2 * prv->Hx) * (prv->Ly + 2 * prv->Hy);
+    T.runmajor = g_tb2_order >= 0 ? g_tb2_order : field_bytes >= 16e9;
     if (!g_tb2_ctr[dev]) return fail(TLB_ERR_STENCIL, "stencil not set on device %d", dev);
     T.ctr = g_tb2_ctr[dev];
     return TLB_OK;

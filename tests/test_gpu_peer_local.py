@@ -229,6 +229,31 @@ def test_peer_pairs_match_oracle(orc, case, arith):
         assert [s for s, _ in res.snapshots] == list(range(every, steps + 1, every))
 
 
+@pytest.mark.parametrize("order", [0, 1])
+def test_peer_pairs_work_orders(orc, order):
+    """The ring two-step kernel with both work orders (interior runs
+    strip-major / run-major) and short runs: bitwise vs the oracle."""
+    import ctypes
+    lib = _lib.load()
+    saved = []
+    for key in (3, 4):
+        v = ctypes.c_int(0)
+        _lib.check(lib.tlb_get_tuning(key, ctypes.byref(v)), "get")
+        saved.append((key, v.value))
+    try:
+        _lib.check(lib.tlb_set_tuning(4, order), "order")
+        _lib.check(lib.tlb_set_tuning(3, 12), "run")
+        p = _params()
+        res = tl.run(tl.SimConfig(Lx=2 * 60, Ly=130, Np=2, tiling="1d", steps=6, params=p,
+                                  init="rayleigh-taylor", exchange="p2p", devices=(0,),
+                                  temporal="on"))
+        want, _ = _oracle(orc, 120, 130, 6, p, False)
+        assert np.array_equal(res.populations, want)
+    finally:
+        for key, v in saved:
+            _lib.check(lib.tlb_set_tuning(key, v), "restore")
+
+
 def test_peer_pairs_are_the_kernel_used():
     """temporal="on" ranks on a 1-D ring allocate 6 halo columns and pair."""
     vs = _vs()

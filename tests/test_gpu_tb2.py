@@ -136,6 +136,30 @@ def test_step2_every_shape_config_bitwise(orc, tb2_tuning, cfg):
         assert [int(s.negatives) for s in stat] == [int(v) for v in np.asarray(neg)[:4]]
 
 
+@pytest.mark.parametrize("order", [0, 1])
+def test_step2_work_orders_bitwise(orc, tb2_tuning, order):
+    """Both work orders of the two-step kernel (strip-major, run-major; the
+    default picks run-major for fields >= 16 GB): exact bitwise vs the
+    oracle, short runs so the order matters."""
+    lib = tb2_tuning
+    old = ctypes.c_int(0)
+    _lib.check(lib.tlb_get_tuning(4, ctypes.byref(old)), "get")
+    try:
+        _lib.check(lib.tlb_set_tuning(4, order), "order")
+        _lib.check(lib.tlb_set_tuning(3, 16), "run")
+        for Lx, Ly, init, periodic in ((256, 300, "rt", False), (96, 245, "random", True)):
+            vs, g, prv, nxt, f0 = _setup(Lx, Ly, init, periodic)
+            p = _params(vs, "exact")
+            got, stat = _run2(vs, g, prv, nxt, p, periodic, 4)
+            orc.set_stencil(vs.c, vs.w, vs.cs2)
+            want, neg = orc.run(f0, 4, orc.params6(p.tau, p.gx, p.gy, p.dt, p.Twall_top,
+                                                   p.Twall_bot),
+                                ymode="periodic" if periodic else "walls")
+            assert np.array_equal(got, want), (order, Lx, Ly)
+    finally:
+        _lib.check(lib.tlb_set_tuning(4, old.value), "order")
+
+
 @pytest.mark.parametrize("layout", ["column", "soa", "aos"])
 def test_step2_equals_single_steps(layout):
     """Two steps in one launch == two fused launches, bitwise, for every

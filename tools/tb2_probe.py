@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--arith", default="fast,exact")
     ap.add_argument("--preload", type=float, default=2.0)
+    ap.add_argument("--order", default="0", help="work orders (TLB_TUNE_TB2_ORDER)")
     ap.add_argument("--cfg", default="1", help="two-step kernel shapes to try (TLB_TUNE_TB2_CFG)")
     ap.add_argument("--run", default="0",
                     help="columns per work item (TLB_TUNE_TB2_RUN, 0 = auto)")
@@ -64,12 +65,15 @@ def main():
         variants = [("single", one, None)]
         for cfg in a.cfg.split(","):
             for run in a.run.split(","):
-                variants.append((f"two_cfg{cfg}_run{run}", two, (int(cfg), int(run))))
+                for order in a.order.split(","):
+                    variants.append((f"two_cfg{cfg}_run{run}_o{order}", two,
+                                     (int(cfg), int(run), int(order))))
         variants.append(("single_again", one, None))
         for name, fn, tune in variants:
             if tune:
                 _lib.check(lib.tlb_set_tuning(2, tune[0]), "cfg")
                 _lib.check(lib.tlb_set_tuning(3, tune[1]), "run")
+                _lib.check(lib.tlb_set_tuning(4, tune[2]), "order")
             fn(10)
             torch.cuda.synchronize()
             t0 = time.time()
