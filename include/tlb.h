@@ -349,7 +349,9 @@ int tlb_pgm_image(const double *v, int64_t nx, int64_t ny, int64_t ld,
 #define TLB_TUNE_MINBLOCKS 1
 #define TLB_TUNE_TB2_CFG 2   /* two-step kernel shape (rows x columns per iteration,
                                 CTAs/SM): 0 = 128 x 2, 1; 1 = 64 x 2, 2 (default);
-                                2 = 96 x 2, 1; 3-6 warp-specialised variants */
+                                2 = 96 x 2, 1; 3-6 warp-specialised variants;
+                                7 = 64 x 2, 2, one site on two threads (fast
+                                arithmetic; exact runs shape 1) */
 #define TLB_TUNE_TB2_RUN 3   /* two-step kernel: columns per work item (0 = chosen
                                 per lattice to fill whole waves; default) */
 #define TLB_TUNE_TB2_ORDER 4 /* two-step kernel work order: -1 auto (default: run-major

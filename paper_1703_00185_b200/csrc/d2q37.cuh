@@ -560,6 +560,108 @@ __device__ __forceinline__ unsigned collide_fast(F &f, const Phys &P) {
     return collide_fast2<ORDER, F, F>(f, f, P);
 }
 
+// ------------------------------------------ fast, one site on two threads --
+// The split two-step kernel (tb2.cu, k_tb2s) runs a site on two threads, one
+// in each warp of a pair: half 0 owns the shells (0,0) (1,0) (1,1) (2,0)
+// (3,0) -- 17 populations, 5 shell set-ups, 8 +/-c pairs -- and half 1 the
+// shells (2,1) (2,2) (3,1) -- 20 populations, 3 set-ups, 10 pairs (about the
+// same FP64 work).  Each half sums its shells' moments, the pair exchanges
+// the partial sums (XCH::sum: own + partner's, the same IEEE sum in both
+// threads), and each half relaxes only its own populations.  Same algebra as
+// collide_fast; the moment sums are grouped differently (1e-12 contract).
+__host__ __device__ constexpr bool HALF_SHELL(int h, int sh) {
+    return (sh == 0 || sh == 1 || sh == 2 || sh == 3 || sh == 6) == (h == 0);
+}
+__host__ __device__ constexpr bool IN_HALF(int h, int l) { return HALF_SHELL(h, SHELL_OF(l)); }
+
+template <int H, class FM>
+__device__ __forceinline__ void fast_moments_half(const FM &fm, double (&m)[4]) {
+    if constexpr (H == 0) {
+        double S1, S2, S3, S6, x1, x2, x3, x6, y1, y2, y3, y6;
+        fast_shell_moments<1>(fm, S1, x1, y1);
+        fast_shell_moments<2>(fm, S2, x2, y2);
+        fast_shell_moments<3>(fm, S3, x3, y3);
+        fast_shell_moments<6>(fm, S6, x6, y6);
+        m[0] = ((fm.get(0) + S1) + (S2 + S3)) + S6;
+        m[1] = (x1 + x2) + (x3 + x6);
+        m[2] = (y1 + y2) + (y3 + y6);
+        m[3] = fma(9.0, S6, fma(4.0, S3, fma(2.0, S2, S1)));   // |c|^2 = 1, 2, 4, 9
+    } else {
+        double S4, S5, S7, x4, x5, x7, y4, y5, y7;
+        fast_shell_moments<4>(fm, S4, x4, y4);
+        fast_shell_moments<5>(fm, S5, x5, y5);
+        fast_shell_moments<7>(fm, S7, x7, y7);
+        m[0] = (S4 + S5) + S7;
+        m[1] = (x4 + x5) + x7;
+        m[2] = (y4 + y5) + y7;
+        m[3] = fma(10.0, S7, fma(8.0, S5, 5.0 * S4));         // |c|^2 = 5, 8, 10
+    }
+}
+
+template <int H, int ORDER, int MODE, class F>
+__device__ __forceinline__ void fast_all_half(F &f, const FastSite &e, double omr) {
+    FastQ k{};
+    if constexpr (ORDER >= 4) k = fast_q(e);
+    if constexpr (H == 0) {
+        fast_shell<ORDER, MODE, 0, F>(f, e, k, omr);
+        fast_shell<ORDER, MODE, 1, F>(f, e, k, omr);
+        fast_shell<ORDER, MODE, 2, F>(f, e, k, omr);
+        fast_shell<ORDER, MODE, 3, F>(f, e, k, omr);
+        fast_shell<ORDER, MODE, 6, F>(f, e, k, omr);
+    } else {
+        fast_shell<ORDER, MODE, 4, F>(f, e, k, omr);
+        fast_shell<ORDER, MODE, 5, F>(f, e, k, omr);
+        fast_shell<ORDER, MODE, 7, F>(f, e, k, omr);
+    }
+}
+
+// collide_fast2 for half H; every thread of both warps must call it (the
+// exchange is a pair barrier).  The failure bits are the same in both halves.
+template <int H, int ORDER, class F, class XCH>
+__device__ __forceinline__ unsigned collide_fast_half(F &f, const Phys &P, XCH &x) {
+    double m[4];
+    fast_moments_half<H>(f, m);
+    x.template sum<4>(m, 0);
+    const double rho = m[0];
+    if (!(rho > 0.0)) return 1u;
+    const double ri = 1.0 / rho;
+    const double ux = m[1] * ri, uy = m[2] * ri;
+    const double T = 0.5 * ri * fma(-rho, fma(ux, ux, uy * uy), m[3]);
+    FastSite e;
+    e.vx = (ux + P.K1) * C.rcs;
+    e.vy = (uy + P.K2) * C.rcs;
+    const double Tb = T - P.K3;
+    if (!(Tb > 0.0)) return 2u;
+    e.theta = fma(Tb, C.rcs2, -1.0);
+    e.s = fma(e.vx, e.vx, e.vy * e.vy);
+    e.W = P.omega * rho;
+    fast_all_half<H, ORDER, 1, F>(f, e, 1.0 - P.omega);
+    return 0u;
+}
+
+// bc_fast for half H: the partial rho is exchanged by every thread (exchange
+// slot `slot`), the wall equilibrium applied only where `on`.
+template <int H, int ORDER, class F, class XCH>
+__device__ __forceinline__ unsigned bc_fast_half(F &f, double Tw, XCH &x, int slot, bool on) {
+    double r0 = 0.0, r1 = 0.0;
+#pragma unroll
+    for (int l = 0; l < Q; ++l) {
+        if (!IN_HALF(H, l)) continue;
+        const double fl = f.get(l);
+        if (l & 1) r1 += fl; else r0 += fl;
+    }
+    double v[1] = {r0 + r1};
+    x.template sum<1>(v, slot);
+    if (!on) return 0u;
+    const double rho = v[0];
+    FastSite e;
+    e.vx = 0.0; e.vy = 0.0; e.s = 0.0;
+    e.theta = fma(Tw, C.rcs2, -1.0);
+    e.W = rho;
+    fast_all_half<H, ORDER, 0, F>(f, e, 0.0);
+    return (rho > 0.0) ? 0u : 4u;
+}
+
 template <int ORDER, class F>
 __device__ __forceinline__ unsigned bc_fast(F &f, double Tw) {
     double r0 = 0.0, r1 = 0.0;

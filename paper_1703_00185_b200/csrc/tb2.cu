@@ -548,6 +548,275 @@ static cudaError_t launch_cfg(const TbLaunch &T, int sms, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+// ------------------------------------------ split variant (fast, cfg 7) --
+// The 64 x 2 kernel holds a whole site (37 populations in flight for the
+// next level-0 column plus 37 for level 2) in 252 registers, so only 8 warps
+// fit an SM and the FP64 chains stall on latency (profiles/r02_tb2.md).
+// Here a site runs on two threads, one in each warp of a pair (warps 2p and
+// 2p+1 hold the same 32 sites): half h owns the populations IN_HALF(h, l)
+// (d2q37.cuh: 17 / 20 of them, about the same FP64 work), gathers, relaxes
+// and stores only those, and the pair exchanges its partial moments through
+// shared memory at a named barrier (ids 1-4).  At <= 128 registers two CTAs
+// of 8 warps fit an SM: 16 warps, the same ring and strip geometry.
+//
+// Every thread of a pair must reach each exchange, so the per-row conditions
+// only predicate stores and reports: threads on rows without work compute
+// on whatever they hold (ring reads stay inside the 3-double pads).
+constexpr int XSLOTS = 6;   // exchange slots: 4 moments, bottom and top wall rho
+
+struct PairX {
+    double *mine, *theirs;  // this thread's column of its half's / the partner's slots
+    int pair;               // named barrier 1 + pair (immediate ids: ptxas then
+                            // reserves 5 barriers per CTA, not all 16)
+    template <int N>
+    __device__ __forceinline__ void sum(double (&v)[N], int slot) {
+#pragma unroll
+        for (int k = 0; k < N; ++k) mine[(slot + k) * 32] = v[k];
+        switch (pair) {
+        case 0: asm volatile("bar.sync 1, 64;" ::: "memory"); break;
+        case 1: asm volatile("bar.sync 2, 64;" ::: "memory"); break;
+        case 2: asm volatile("bar.sync 3, 64;" ::: "memory"); break;
+        default: asm volatile("bar.sync 4, 64;" ::: "memory"); break;
+        }
+#pragma unroll
+        for (int k = 0; k < N; ++k) v[k] += theirs[(slot + k) * 32];
+    }
+};
+
+// RingPut / GlobalPut for one half: the slow negatives recount covers only
+// the half's own populations
+template <int ROWS, int LANES, int H>
+struct RingPutH : RingPut<ROWS, LANES> {
+    __device__ __forceinline__ unsigned negatives() const {
+        if ((int)this->sgn >= 0) return 0u;
+        unsigned n = 0;
+#define TLB_RG(L) if (IN_HALF(H, L)) n += this->row[slot_of<LANES, L>(this->ws) * ROWS] < 0.0;
+        TLB_RG(0) TLB_RG(1) TLB_RG(2) TLB_RG(3) TLB_RG(4) TLB_RG(5) TLB_RG(6) TLB_RG(7)
+        TLB_RG(8) TLB_RG(9) TLB_RG(10) TLB_RG(11) TLB_RG(12) TLB_RG(13) TLB_RG(14)
+        TLB_RG(15) TLB_RG(16) TLB_RG(17) TLB_RG(18) TLB_RG(19) TLB_RG(20) TLB_RG(21)
+        TLB_RG(22) TLB_RG(23) TLB_RG(24) TLB_RG(25) TLB_RG(26) TLB_RG(27) TLB_RG(28)
+        TLB_RG(29) TLB_RG(30) TLB_RG(31) TLB_RG(32) TLB_RG(33) TLB_RG(34) TLB_RG(35)
+        TLB_RG(36)
+#undef TLB_RG
+        return n;
+    }
+};
+
+template <int H>
+struct GlobalPutH {
+    double (&a)[Q];
+    char *dp;
+    const long long *doffb;
+    unsigned sgn;
+    bool on;                // this thread's row is an output row
+    __device__ __forceinline__ double get(int l) const { return a[l]; }
+    __device__ __forceinline__ void put(int l, double v) {
+        // a predicated store, not a branch per population
+        asm volatile("{ .reg .pred p; setp.ne.u32 p, %2, 0; @p st.global.f64 [%0], %1; }" ::"l"(
+                         dp + doffb[l]), "d"(v), "r"((unsigned)on) : "memory");
+        sgn = sign_or(sgn, v);
+    }
+    __device__ __forceinline__ unsigned negatives() const {
+        if ((int)sgn >= 0) return 0u;
+        unsigned n = 0;
+#pragma unroll 1
+        for (int l = 0; l < Q; ++l)
+            if (IN_HALF(H, l)) n += *reinterpret_cast<const volatile double *>(dp + doffb[l]) < 0.0;
+        return n;
+    }
+};
+
+template <int H, int l>
+__device__ __forceinline__ void load_h(double (&f)[Q], const Fld &s, int x, int y, int flags) {
+    if constexpr (IN_HALF(H, l)) load_one<l, false>(f, s, x, y, true, true, flags);
+}
+template <int H, int... Ls>
+struct LoadHalf {
+    __device__ __forceinline__ static void run(double (&f)[Q], const Fld &s, int x, int y,
+                                               int flags) {
+        (load_h<H, Ls>(f, s, x, y, flags), ...);
+    }
+};
+
+template <int H>
+__device__ __forceinline__ void gather0_half(double (&f)[Q], const TbLaunch &T, int x, int y) {
+    const Fld &S = T.src;
+    const bool inner = x >= S.Hx + 3 && x < S.Hx + S.Lx - 3 && y >= S.Hy + 3 &&
+                       y < S.Hy + S.Ly - 3;
+    if (inner) {
+        const char *sp = reinterpret_cast<const char *>(S.base + (long long)x * S.sx +
+                                                        (long long)y * S.sy);
+#pragma unroll
+        for (int l = 0; l < Q; ++l)
+            if (IN_HALF(H, l)) f[l] = __ldg(reinterpret_cast<const double *>(sp + T.soffb[l]));
+    } else {
+        LoadHalf<H, 0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16, 17, 18, 19, 20, 21,
+                 22, 23, 24, 25, 26, 27, 28, 29, 30, 31, 32, 33, 34, 35, 36>::run(f, S, x, y,
+                                                                                  T.flags);
+    }
+}
+
+template <int ROWS, int LANES, int l>
+__device__ __forceinline__ void ring_get_h(double (&g)[Q], const double *row, const int (&rs)[7]) {
+    g[l] = row[slot_of<LANES, l>(rs) * ROWS - CY(l)];
+}
+template <int H, int ROWS, int LANES, int... Ls>
+struct RingGetHalf {
+    __device__ __forceinline__ static void run(double (&g)[Q], const double *row,
+                                               const int (&rs)[7]) {
+        ((IN_HALF(H, Ls) ? ring_get_h<ROWS, LANES, Ls>(g, row, rs) : void()), ...);
+    }
+};
+
+// bc on the wall rows of a wall strip: every thread exchanges (both sides,
+// bottom then top like bc(), kernels.py:190-203), the rows in range apply
+template <int H>
+__device__ __forceinline__ unsigned walls_half(double (&f)[Q], const TbLaunch &T, int y,
+                                               PairX &x) {
+    unsigned bits = 0;
+    const bool bot = y >= T.bot_lo && y < T.bot_hi;
+    const bool top = y >= T.top_lo && y < T.top_hi;
+    RegF rf{f};
+    bits |= bc_fast_half<H, 4>(rf, T.P.Tbot, x, 4, bot);
+    bits |= bc_fast_half<H, 4>(rf, T.P.Ttop, x, 5, top);
+    return bits;
+}
+
+template <int H, int ROWS, int LANES, bool PF>
+__device__ __forceinline__ void tb2s_body(const TbLaunch &T, double *ring, PairX &px, int lane,
+                                          int r, long long &s_item, unsigned &neg1,
+                                          unsigned &neg2) {
+    const Fld &S = T.src;
+    const int Lx = S.Lx, Ly = S.Ly, Hx = S.Hx, Hy = S.Hy;
+    double *row = ring + r;
+    for (;;) {
+        if (threadIdx.x == 0) s_item = (long long)atomicAdd(T.ctr, 1u);
+        __syncthreads();
+        const long long item = s_item;
+        if (item >= T.items) break;
+        int strip, xa, xb;
+        item_of(T, item, strip, xa, xb);
+        const int ys = Hy + (int)((long long)Ly * strip / T.ns);
+        const int hs = Hy + (int)((long long)Ly * (strip + 1) / T.ns) - ys;
+        const int y1 = ys - 3 + r;
+        const bool row1 = r < hs + 6;
+        int y1s = y1;
+        if (T.flags & TLB_F_WRAP_Y) {
+            if (y1s < Hy) y1s += Ly;
+            else if (y1s >= Hy + Ly) y1s -= Ly;
+        } else {
+            y1s = y1s < Hy ? Hy : (y1s >= Hy + Ly ? Hy + Ly - 1 : y1s);
+        }
+        const bool row2 = r >= 3 && r < hs + 3;
+        // the strip's level-1 rows (clamped like y1s) meet a wall range:
+        // uniform over the CTA, so the wall exchanges are too
+        int lo = ys - 3, hi = ys + hs + 3;
+        if (!(T.flags & TLB_F_WRAP_Y)) {
+            lo = lo < Hy ? Hy : lo;
+            hi = hi > Hy + Ly ? Hy + Ly : hi;
+        }
+        const bool wall = (lo < T.bot_hi && hi > T.bot_lo) || (lo < T.top_hi && hi > T.top_lo);
+        const int K = (xb - xa + 6 + LANES - 1) / LANES;
+        auto wrapx = [&](int x) { return x < Hx ? x + Lx : (x >= Hx + Lx ? x - Lx : x); };
+        double f[Q];
+        if (PF && row1) gather0_half<H>(f, T, wrapx(xa - 3 + lane), y1s);
+        int ws[7], rs[7];
+#pragma unroll
+        for (int c = -3; c <= 3; ++c) {
+            ws[c + 3] = lane % GD<LANES>(c);
+            rs[c + 3] = (lane + 2 * GD<LANES>(c) - 3 - c) % GD<LANES>(c);
+        }
+        for (int k = 0; k < K; ++k) {
+            const int j = LANES * k + lane;
+            const int X1 = xa - 3 + j;
+            if (X1 < xb + 3) {   // uniform over a warp (one column)
+                if (!PF && row1) gather0_half<H>(f, T, wrapx(X1), y1s);
+                unsigned bits = wall ? walls_half<H>(f, T, y1s, px) : 0u;
+                RingPutH<ROWS, LANES, H> rp{{f, row, ws, 0u}};
+                bits |= collide_fast_half<H, 4>(rp, T.P, px);
+                if (H == 0 && row1 && bits) report(T.st1, bits, wrapx(X1), y1s, T.step);
+                if (row2 && X1 >= xa && X1 < xb) neg1 += rp.negatives();
+            }
+            if (PF && row1 && k + 1 < K && X1 + LANES < xb + 3)
+                gather0_half<H>(f, T, wrapx(X1 + LANES), y1s);
+            __syncthreads();
+            const int X2 = X1 - 3;
+            if (X2 >= xa && X2 < xb) {   // uniform over a warp
+                double g[Q];
+                RingGetHalf<H, ROWS, LANES, 0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15,
+                            16, 17, 18, 19, 20, 21, 22, 23, 24, 25, 26, 27, 28, 29, 30, 31, 32,
+                            33, 34, 35, 36>::run(g, row, rs);
+                unsigned bits = wall ? walls_half<H>(g, T, y1, px) : 0u;
+                char *dp = reinterpret_cast<char *>(T.dst.base + (long long)X2 * T.dst.sx +
+                                                    (long long)y1 * T.dst.sy);
+                GlobalPutH<H> gp{g, dp, T.doffb, 0u, row2};
+                bits |= collide_fast_half<H, 4>(gp, T.P, px);
+                if (row2) {
+                    neg2 += gp.negatives();
+                    if (H == 0 && bits) report(T.st2, bits, X2, y1, T.step + 1);
+                }
+            }
+#pragma unroll
+            for (int c = -3; c <= 3; ++c) {
+                ws[c + 3] += LANES;
+                if (ws[c + 3] >= GD<LANES>(c)) ws[c + 3] -= GD<LANES>(c);
+                rs[c + 3] += LANES;
+                if (rs[c + 3] >= GD<LANES>(c)) rs[c + 3] -= GD<LANES>(c);
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// shared memory: [3 pad][ring][3 pad][exchange: one XSLOTS x 32 block per warp
+// (ROWS * LANES / 32 pairs x 2 halves)]
+template <int ROWS, int LANES>
+constexpr size_t split_smem() {
+    return ((size_t)slots(LANES) * ROWS + 6 + (size_t)(2 * ROWS * LANES / 32) * XSLOTS * 32) *
+           sizeof(double);
+}
+
+// PF: the next level-0 column is gathered into registers during level 2
+template <int ROWS, int LANES, int MINB, bool PF>
+__global__ void __launch_bounds__(2 * ROWS * LANES, MINB) k_tb2s(const __grid_constant__ TbLaunch T) {
+    static_assert(ROWS % 32 == 0, "a warp covers 32 rows of one column");
+    extern __shared__ double smem[];
+    double *ring = smem + 3;
+    double *xch = smem + slots(LANES) * ROWS + 6;
+    const int warp = threadIdx.x / 32, h = warp & 1, p = warp >> 1;
+    const int site = p * 32 + (threadIdx.x & 31);
+    const int lane = site / ROWS, r = site % ROWS;
+    double *col = xch + (size_t)p * 2 * XSLOTS * 32 + (threadIdx.x & 31);
+    PairX px{col + h * XSLOTS * 32, col + (1 - h) * XSLOTS * 32, p};
+    __shared__ long long s_item;
+    unsigned neg1 = 0, neg2 = 0;
+    if (h == 0) tb2s_body<0, ROWS, LANES, PF>(T, ring, px, lane, r, s_item, neg1, neg2);
+    else tb2s_body<1, ROWS, LANES, PF>(T, ring, px, lane, r, s_item, neg1, neg2);
+    if (T.flags & TLB_F_COUNT_NEG) {
+        count_neg_n(T.st1, neg1);
+        count_neg_n(T.st2, neg2);
+    }
+}
+
+template <int ROWS, int LANES, int MINB, bool PF>
+static cudaError_t launch_split(const TbLaunch &T, int sms, cudaStream_t s) {
+    const size_t smem = split_smem<ROWS, LANES>();
+    static bool attr[64] = {};
+    int dev = 0;
+    cudaError_t e0 = cudaGetDevice(&dev);
+    if (e0 != cudaSuccess) return e0;
+    auto *fn = k_tb2s<ROWS, LANES, MINB, PF>;
+    if (dev < 0 || dev >= 64 || !attr[dev]) {
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+        if (dev >= 0 && dev < 64) attr[dev] = true;
+    }
+    long long grid = (long long)sms * MINB;
+    if (grid > T.items) grid = T.items;
+    fn<<<(unsigned)grid, 2 * ROWS * LANES, smem, s>>>(T);
+    return cudaGetLastError();
+}
 
 // ------------------------------------------------ warp-specialised variant --
 // Producer warps (level 1: HBM gather, bc + collide, ring) and consumer warps
@@ -706,7 +975,7 @@ cudaError_t tb2_set_const(const StencilConst &h) {
 }
 
 int tb2_rows(int cfg) {
-    return (cfg == 1 || cfg == 4) ? 64 : (cfg == 2 || cfg == 6) ? 96 : 128;
+    return (cfg == 1 || cfg == 4 || cfg == 7 || cfg == 8) ? 64 : (cfg == 2 || cfg == 6) ? 96 : 128;
 }
 
 cudaError_t tb2_launch_peer(const tb2::TbLaunch &T0, bool exact, int sms, cudaStream_t s) {
@@ -745,6 +1014,14 @@ cudaError_t tb2_launch(const tb2::TbLaunch &T, bool exact, int cfg, int sms, cud
     case 6:
         return exact ? tb2::launch_ws<true, 96, 2, 2, 8, 1>(T, sms, s)
                      : tb2::launch_ws<false, 96, 2, 2, 8, 1>(T, sms, s);
+    // split (fast only: exact's fixed-order sums cannot be split; it runs
+    // the 64 x 2 kernel of cfg 1)
+    case 7:
+        return exact ? tb2::launch_cfg<true, 64, 2, 2>(T, sms, s)
+                     : tb2::launch_split<64, 2, 2, true>(T, sms, s);
+    case 8:
+        return exact ? tb2::launch_cfg<true, 64, 2, 2>(T, sms, s)
+                     : tb2::launch_split<64, 2, 2, false>(T, sms, s);
     default:
         return exact ? tb2::launch_cfg<true, 128, 2, 1>(T, sms, s)
                      : tb2::launch_cfg<false, 128, 2, 1>(T, sms, s);

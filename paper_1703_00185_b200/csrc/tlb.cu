@@ -596,7 +596,7 @@ int tlb_version(void) { return 1; }
 
 int tlb_set_tuning(int key, int value) {
     if (key == TLB_TUNE_TB2_CFG) {
-        if (value < 0 || value > 6) return fail(TLB_ERR_CONTRACT, "two-step config must be 0-6");
+        if (value < 0 || value > 8) return fail(TLB_ERR_CONTRACT, "two-step config must be 0-8");
         g_tb2_cfg = value;
         return TLB_OK;
     }
@@ -918,7 +918,7 @@ static int tb2_setup(tb2::TbLaunch &T, const TlbField *prv, const TlbField *nxt,
     // work items: runs of run_l columns of a strip; wall strips (bc rows)
     // first, in runs of half the length
     const int Lx = prv->Lx;
-    T.run_l = tb2_run_length(Lx, T.ns, walls, sms * (cfg == 1 ? 2 : 1));
+    T.run_l = tb2_run_length(Lx, T.ns, walls, sms * ((cfg == 1 || cfg >= 7) ? 2 : 1));
     if ((Lx + T.run_l - 1) / T.run_l < min_runs) T.run_l = (Lx + min_runs - 1) / min_runs;
     T.run_h = T.run_l / 2 > 8 ? T.run_l / 2 : T.run_l;
     T.nheavy = walls ? (T.ns >= 2 ? 2 : 1) : 0;

@@ -112,7 +112,7 @@ def tb2_tuning():
         _lib.check(lib.tlb_set_tuning(key, v), "set_tuning")
 
 
-@pytest.mark.parametrize("cfg", range(7))
+@pytest.mark.parametrize("cfg", range(9))
 def test_step2_every_shape_config_bitwise(orc, tb2_tuning, cfg):
     """Every compiled two-step kernel shape (rows x columns, CTAs/SM,
     warp-specialised) and work items from 8 columns to whole strips: exact
@@ -134,6 +134,63 @@ def test_step2_every_shape_config_bitwise(orc, tb2_tuning, cfg):
                             ymode="periodic" if periodic else "walls")
         assert np.array_equal(got, want), (cfg, Lx, Ly)
         assert [int(s.negatives) for s in stat] == [int(v) for v in np.asarray(neg)[:4]]
+
+
+SPLIT_CFGS = (7, 8)   # one site on two threads (tb2.cu k_tb2s), fast arithmetic
+
+
+@pytest.mark.parametrize("cfg", SPLIT_CFGS)
+@pytest.mark.parametrize("shape", SHAPES + [(96, 300, "random", False), (256, 300, "rt", False)],
+                         ids=lambda s: f"{s[0]}x{s[1]}-{s[2]}-{s[3]}")
+def test_step2_split_fast_vs_oracle(orc, tb2_tuning, shape, cfg):
+    """The split two-step kernel (one site on a pair of warps, partial
+    moments exchanged at a named barrier): fast arithmetic within 1e-12 of
+    the oracle over 6 steps, per-step negatives and flags equal; short runs
+    (16 columns) and whole strips."""
+    lib = tb2_tuning
+    _lib.check(lib.tlb_set_tuning(2, cfg), "cfg")
+    Lx, Ly, init, periodic = shape
+    for run in (16, 0):
+        _lib.check(lib.tlb_set_tuning(3, run), "run")
+        vs, g, prv, nxt, f0 = _setup(Lx, Ly, init, periodic)
+        p = _params(vs, "fast")
+        got, stat = _run2(vs, g, prv, nxt, p, periodic, 6)
+        orc.set_stencil(vs.c, vs.w, vs.cs2)
+        want, neg = orc.run(f0, 6, orc.params6(p.tau, p.gx, p.gy, p.dt, p.Twall_top,
+                                               p.Twall_bot),
+                            ymode="periodic" if periodic else "walls")
+        assert np.max(np.abs(got - want) / np.abs(want)) < 1e-12, (shape, run)
+        assert [int(s.negatives) for s in stat] == [int(v) for v in np.asarray(neg)[:6]]
+        assert all(s.flags == 0 for s in stat)
+
+
+@pytest.mark.parametrize("cfg", SPLIT_CFGS)
+def test_step2_split_c2_vs_fused(tb2_tuning, cfg):
+    """configs[1] (1920x2048): 10 split two-step launches vs 20 fused steps,
+    fast arithmetic, 1e-12; negatives per step equal."""
+    lib = tb2_tuning
+    _lib.check(lib.tlb_set_tuning(2, cfg), "cfg")
+    vs, g, prv, nxt, _ = _setup(1920, 2048, "rt", False)
+    p = _params(vs, "fast")
+    state = prv.data.clone()
+    two, s2 = _run2(vs, g, prv, nxt, p, False, 20, two=True)
+    prv.data.copy_(state)
+    one, s1 = _run2(vs, g, prv, nxt, p, False, 20, two=False)
+    del state
+    assert np.max(np.abs(two - one) / np.abs(one)) < 1e-12
+    assert [s.negatives for s in s2] == [s.negatives for s in s1]
+
+
+@pytest.mark.parametrize("cfg", SPLIT_CFGS)
+def test_step2_split_reports_failures(tb2_tuning, cfg):
+    """A failing site is reported once, with its step, by the split kernel."""
+    lib = tb2_tuning
+    _lib.check(lib.tlb_set_tuning(2, cfg), "cfg")
+    vs, g, prv, nxt, _ = _setup(64, 64, "random", True)
+    p = _params(vs, "fast")
+    prv.pops[:, g.Hx + 10, g.Hy + 20] = -1.0
+    _, stat = _run2(vs, g, prv, nxt, p, True, 2)
+    assert stat[0].flags & _lib.ST_DEGENERATE
 
 
 @pytest.mark.parametrize("order", [0, 1])

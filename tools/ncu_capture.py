@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--arith", default="fast,exact")
     ap.add_argument("--layout", default="column")
     ap.add_argument("--hash-only", default=None)
+    ap.add_argument("--cfg", type=int, default=None, help="TLB_TUNE_TB2_CFG for the pair launch")
     a = ap.parse_args()
     if a.hash_only:
         import bench
@@ -45,6 +46,8 @@ def main():
     prv.pops[:, g.phys_x, g.phys_y] = tl.equilibrium(
         *[torch.as_tensor(np.ascontiguousarray(m), device="cuda") for m in macro], vs)
     lib = _lib.load()
+    if a.cfg is not None:
+        _lib.check(lib.tlb_set_tuning(2, a.cfg), "cfg")
     st = torch.zeros((2, _lib.STATUS_BYTES), dtype=torch.uint8, device="cuda")
     sp = _lib.stream_ptr()
     for arith in a.arith.split(","):
