@@ -855,9 +855,9 @@ int tlb_step_self(const TlbField *prv, const TlbField *nxt, const TlbParams *p, 
 // 6 warm-up columns of a run), so pick the run that minimises that product
 // (C2: 15 runs of 128 = 570 items on 296 CTAs, 1.93 waves; 16 runs of 120
 // would be 608 items, 3 waves).  An explicit TLB_TUNE_TB2_RUN overrides.
-static int tb2_run_length(int Lx, int ns, bool walls, int ctas) {
+static int tb2_run_length(int Lx, int ns, bool edges, int ctas) {
     if (g_tb2_run > 0) return g_tb2_run < Lx ? g_tb2_run : Lx;
-    const int nheavy = walls ? (ns >= 2 ? 2 : 1) : 0;
+    const int nheavy = edges ? (ns >= 2 ? 2 : 1) : 0;
     long long best = -1;
     int best_run = Lx < 128 ? Lx : 128;
     for (int r = 1; r <= Lx / 32 + 1; ++r) {
@@ -891,6 +891,11 @@ static int tb2_setup(tb2::TbLaunch &T, const TlbField *prv, const TlbField *nxt,
         return fail(TLB_ERR_UNSUPPORTED, "two-step kernel: tile smaller than 8x8");
     if (prv->base == nxt->base) return fail(TLB_ERR_CONTRACT, "step2: prv and nxt alias");
     const bool walls = (flags & TLB_F_WALL_BOT) != 0;
+    // the first and last strips (wall rows, or the periodic wrap of the
+    // level-1 halo rows) are slower per column: they go first, in half runs,
+    // so the schedule does not end on them (periodic C2: 9.0k -> see
+    // profiles/r02_tb2.md)
+    const bool edges = walls || (flags & TLB_F_WRAP_Y) != 0;
     if (walls && (!(p->Twall_top > 0.0) || !(p->Twall_bot > 0.0)))
         return fail(TLB_ERR_DOMAIN, "equilibrium requires rho > 0 and T > 0");
     memset(&T, 0, sizeof T);
@@ -918,11 +923,11 @@ static int tb2_setup(tb2::TbLaunch &T, const TlbField *prv, const TlbField *nxt,
     // work items: runs of run_l columns of a strip; wall strips (bc rows)
     // first, in runs of half the length
     const int Lx = prv->Lx;
-    T.run_l = tb2_run_length(Lx, T.ns, walls, sms * ((cfg == 1 || cfg >= 7) ? 2 : 1));
+    T.run_l = tb2_run_length(Lx, T.ns, edges, sms * ((cfg == 1 || cfg >= 7) ? 2 : 1));
     if ((Lx + T.run_l - 1) / T.run_l < min_runs) T.run_l = (Lx + min_runs - 1) / min_runs;
     T.run_h = T.run_l / 2 > 8 ? T.run_l / 2 : T.run_l;
-    T.nheavy = walls ? (T.ns >= 2 ? 2 : 1) : 0;
-    T.first_light = walls ? 1 : 0;
+    T.nheavy = edges ? (T.ns >= 2 ? 2 : 1) : 0;
+    T.first_light = edges ? 1 : 0;
     const int nlight = T.ns - T.nheavy;
     T.hruns = (Lx + T.run_h - 1) / T.run_h;
     T.lruns = (Lx + T.run_l - 1) / T.run_l;

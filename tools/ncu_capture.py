@@ -22,7 +22,10 @@ def main():
     ap.add_argument("--arith", default="fast,exact")
     ap.add_argument("--layout", default="column")
     ap.add_argument("--hash-only", default=None)
+    ap.add_argument("--periodic", action="store_true", help="periodic Y instead of walls")
+    ap.add_argument("--run", type=int, default=None, help="TLB_TUNE_TB2_RUN")
     ap.add_argument("--cfg", type=int, default=None, help="TLB_TUNE_TB2_CFG for the pair launch")
+    ap.add_argument("--init", default="rayleigh-taylor", help="initial condition preset")
     a = ap.parse_args()
     if a.hash_only:
         import bench
@@ -42,10 +45,13 @@ def main():
     _lib.ensure_stencil(vs, 0)
     g = tl.LatticeGeometry(a.Lx, a.Ly, 3, 3, 37, a.layout)
     prv, nxt = tl.allocate_field(g, vs)
-    macro = tl.init.rayleigh_taylor_macro(a.Lx, a.Ly, vs)
+    macro = (tl.init.rayleigh_taylor_macro(a.Lx, a.Ly, vs) if a.init == "rayleigh-taylor"
+             else tl.init.initial_macro(a.init, a.Lx, a.Ly, vs))
     prv.pops[:, g.phys_x, g.phys_y] = tl.equilibrium(
         *[torch.as_tensor(np.ascontiguousarray(m), device="cuda") for m in macro], vs)
     lib = _lib.load()
+    if a.run is not None:
+        _lib.check(lib.tlb_set_tuning(3, a.run), "run")
     if a.cfg is not None:
         _lib.check(lib.tlb_set_tuning(2, a.cfg), "cfg")
     st = torch.zeros((2, _lib.STATUS_BYTES), dtype=torch.uint8, device="cuda")
@@ -55,10 +61,10 @@ def main():
                                           Twall_bot=1.1 * vs.cs2, arith=arith), vs)
         for what in a.what.split(","):
             if what == "single":
-                _lib.check(lib.tlb_step_self(field_desc(prv), field_desc(nxt), tp, 1, 0, 1,
+                _lib.check(lib.tlb_step_self(field_desc(prv), field_desc(nxt), tp, int(not a.periodic), int(a.periodic), 1,
                                              st[0].data_ptr(), sp), "step")
             else:
-                _lib.check(lib.tlb_step2_self(field_desc(prv), field_desc(nxt), tp, 1, 0, 1,
+                _lib.check(lib.tlb_step2_self(field_desc(prv), field_desc(nxt), tp, int(not a.periodic), int(a.periodic), 1,
                                               st[0].data_ptr(), st[1].data_ptr(), 0, sp),
                            "step2")
             prv, nxt = nxt, prv

@@ -27,21 +27,25 @@ def main():
     ap.add_argument("--arith", default="fast,exact")
     ap.add_argument("--preload", type=float, default=2.0)
     ap.add_argument("--order", default="0", help="work orders (TLB_TUNE_TB2_ORDER)")
+    ap.add_argument("--periodic", action="store_true", help="periodic Y instead of walls")
     ap.add_argument("--cfg", default="1", help="two-step kernel shapes to try (TLB_TUNE_TB2_CFG)")
     ap.add_argument("--run", default="0",
                     help="columns per work item (TLB_TUNE_TB2_RUN, 0 = auto)")
+    ap.add_argument("--init", default="rayleigh-taylor", help="initial condition preset")
     a = ap.parse_args()
     vs = tl.build_velocity_set("D2Q37")
     _lib.ensure_stencil(vs, 0)
     g = tl.LatticeGeometry(a.Lx, a.Ly, 3, 3, 37, "column")
     prv, nxt = tl.allocate_field(g, vs)
-    macro = tl.init.rayleigh_taylor_macro(a.Lx, a.Ly, vs)
+    macro = (tl.init.rayleigh_taylor_macro(a.Lx, a.Ly, vs) if a.init == "rayleigh-taylor"
+             else tl.init.initial_macro(a.init, a.Lx, a.Ly, vs))
     prv.pops[:, g.phys_x, g.phys_y] = tl.equilibrium(
         *[torch.as_tensor(np.ascontiguousarray(m), device="cuda") for m in macro], vs)
     lib = _lib.load()
     st = torch.zeros((2, _lib.STATUS_BYTES), dtype=torch.uint8, device="cuda")
     sp = _lib.stream_ptr()
     sites = a.Lx * a.Ly
+    wl, pe = (0, 1) if a.periodic else (1, 0)
     for arith in a.arith.split(","):
         p = tl.PhysicsParams(tau=0.8, gy=-1e-5, Twall_top=0.9 * vs.cs2,
                              Twall_bot=1.1 * vs.cs2, arith=arith)
@@ -50,13 +54,13 @@ def main():
 
         def one(n):
             for _ in range(n):
-                _lib.check(lib.tlb_step_self(field_desc(bufs[0]), field_desc(bufs[1]), tp, 1, 0,
+                _lib.check(lib.tlb_step_self(field_desc(bufs[0]), field_desc(bufs[1]), tp, wl, pe,
                                              1, st[0].data_ptr(), sp), "step")
                 bufs.reverse()
 
         def two(n):
             for _ in range(n // 2):
-                _lib.check(lib.tlb_step2_self(field_desc(bufs[0]), field_desc(bufs[1]), tp, 1, 0,
+                _lib.check(lib.tlb_step2_self(field_desc(bufs[0]), field_desc(bufs[1]), tp, wl, pe,
                                               1, st[0].data_ptr(), st[1].data_ptr(), 0, sp),
                            "step2")
                 bufs.reverse()
