@@ -863,6 +863,10 @@ static int tb2_run_length(int Lx, int ns, bool edges, int ctas) {
     for (int r = 1; r <= Lx / 32 + 1; ++r) {
         const int run = (Lx + r - 1) / r;
         if (run < 32 && r > 1) break;
+        // runs longer than 512 columns lose 4-8 % on tall tiles whatever the
+        // wave count (4096x8192: 2048 -> 512 columns 13.1k -> 13.9k MLUPS;
+        // 2048x16384 13.3k -> 14.2k; profiles/r02_tb2.md)
+        if (run > 512 && Lx > 512) continue;
         const int run_h = run / 2 > 8 ? run / 2 : run;
         const long long items = (long long)nheavy * ((Lx + run_h - 1) / run_h) +
                                 (long long)(ns - nheavy) * r;
