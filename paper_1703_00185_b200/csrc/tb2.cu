@@ -167,7 +167,11 @@ __device__ __forceinline__ void gather0(double (&f)[Q], const TbLaunch &T, int x
     if (inner) {
         const char *sp = reinterpret_cast<const char *>(S.base + (long long)x * S.sx +
                                                         (long long)y * S.sy);
-        if (coh) {
+        // the ring variant takes the coherent path for every column: one load
+        // sequence the compiler can hoist as a whole (a branch between an
+        // .nc and a .cg copy cost the prefetch its overlap: long_scoreboard
+        // 0.33 -> 1.63 per issue, profiles/r02_tb2.md)
+        if (!XWRAP) {
 #pragma unroll
             for (int l = 0; l < Q; ++l)
                 f[l] = __ldcg(reinterpret_cast<const double *>(sp + T.soffb[l]));
@@ -176,7 +180,7 @@ __device__ __forceinline__ void gather0(double (&f)[Q], const TbLaunch &T, int x
             for (int l = 0; l < Q; ++l)
                 f[l] = __ldg(reinterpret_cast<const double *>(sp + T.soffb[l]));
         }
-    } else if (coh) {
+    } else if (!XWRAP || coh) {
         load_all<1>(f, S, x, y, true, true, T.flags);
     } else {
         load_all<0>(f, S, x, y, true, true, T.flags);
