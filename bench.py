@@ -541,6 +541,16 @@ def gpu_arm(args, rank, world, local_rank):
              "k_site<3, %d, 4, 0, 4>" % (1 if args.arith == "exact" else 0) if world == 1 else
              "k_peer_step<%d, 0>" % (1 if args.arith == "exact" else 0))
     traffic, traffic_src = ncu_traffic(kname, args.layout)
+    # the committed captures are of the configs[1] tile (1920x2048 per GPU):
+    # another tile size gets the capture's bytes per site, not a per-launch
+    # figure of a different launch
+    traffic_site = None
+    if traffic is not None:
+        traffic_site = round(traffic * 1e9 / (TILE_LX * TILE_LY), 1)
+        if (Lx_tile, Ly_tile) != (TILE_LX, TILE_LY):
+            traffic = None
+            traffic_src += ("; captured on the %dx%d tile: only its bytes per site apply"
+                            % (TILE_LX, TILE_LY))
     out = None
     if rank == 0:
         lib = _lib.load()
@@ -579,6 +589,7 @@ def gpu_arm(args, rank, world, local_rank):
                          "unit": "GB/s", "frac": round(achieved / hbm_peak, 4),
                          "traffic": traffic, "traffic_unit": "GB per launch (ncu dram read+write)",
                          "traffic_source": traffic_src,
+                         "traffic_B_per_site": traffic_site,
                          "algorithmic_bytes_per_launch_GB": round(BYTES_SITE * kern_sites / 1e9, 4),
                          "kernel": (kname + " (TWO steps per launch: propagate+bc+collide "
                                     "twice, the intermediate state in shared memory)") if pair
