@@ -355,7 +355,7 @@ int tlb_pgm_image(const double *v, int64_t nx, int64_t ny, int64_t ld,
 #define TLB_TUNE_TB2_RUN 3   /* two-step kernel: columns per work item (0 = chosen
                                 per lattice to fill whole waves; default) */
 #define TLB_TUNE_TB2_ORDER 4 /* two-step kernel work order: -1 auto (default: run-major
-                                for fields >= 16 GB), 0 strip-major, 1 run-major
+                                for fields >= 4 GB), 0 strip-major, 1 run-major
                                 (all strips at one X range first) */
 int tlb_set_tuning(int key, int value);
 /* Current value of a tuning knob. */

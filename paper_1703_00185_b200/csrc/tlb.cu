@@ -936,11 +936,12 @@ static int tb2_setup(tb2::TbLaunch &T, const TlbField *prv, const TlbField *nxt,
     T.hruns = (Lx + T.run_h - 1) / T.run_h;
     T.lruns = (Lx + T.run_l - 1) / T.run_l;
     T.items = (long long)T.nheavy * T.hruns + (long long)nlight * T.lruns;
-    // work order: run-major on huge tiles, where strip-major puts the ~300
-    // concurrent runs all over a tens-of-GB buffer (address translation:
-    // 8192x16384 +18 %; C2 +1 %, C5 -1 %; profiles/r02_tb2.md)
+    // work order: run-major on large tiles, where strip-major puts the ~300
+    // concurrent runs all over a multi-GB buffer (with runs of <= 512
+    // columns: 4096x8192 +4 %, 2048x16384 +2.4 %, 4096x16384 +12 %,
+    // 8192x16384 +18 %; C2 within noise; profiles/r02_tb2.md)
     const double field_bytes = 8.0 * Q * (double)(prv->Lx + 2 * prv->Hx) * (prv->Ly + 2 * prv->Hy);
-    T.runmajor = g_tb2_order >= 0 ? g_tb2_order : field_bytes >= 16e9;
+    T.runmajor = g_tb2_order >= 0 ? g_tb2_order : field_bytes >= 4e9;
     if (!g_tb2_ctr[dev]) return fail(TLB_ERR_STENCIL, "stencil not set on device %d", dev);
     T.ctr = g_tb2_ctr[dev];
     return TLB_OK;
