@@ -246,16 +246,18 @@ def test_step2_reports_failures_with_their_step():
     assert stat[0].flags & _lib.ST_DEGENERATE
 
 
-def test_step2_c2_fast_and_exact_vs_fused():
-    """The BASELINE configs[1] lattice (1920x2048): 10 two-step launches
-    equal 20 fused steps (exact bitwise, fast 1e-12)."""
+@pytest.mark.parametrize("periodic", [False, True])
+def test_step2_c2_fast_and_exact_vs_fused(periodic):
+    """The BASELINE configs[1] lattice (1920x2048), walls and periodic Y
+    (whose wrap strips the schedule runs first): 10 two-step launches equal
+    20 fused steps (exact bitwise, fast 1e-12)."""
     for arith in ("exact", "fast"):
-        vs, g, prv, nxt, _ = _setup(1920, 2048, "rt", False)
+        vs, g, prv, nxt, _ = _setup(1920, 2048, "rt", periodic)
         p = _params(vs, arith)
         state = prv.data.clone()
-        two, s2 = _run2(vs, g, prv, nxt, p, False, 20, two=True)
+        two, s2 = _run2(vs, g, prv, nxt, p, periodic, 20, two=True)
         prv.data.copy_(state)
-        one, s1 = _run2(vs, g, prv, nxt, p, False, 20, two=False)
+        one, s1 = _run2(vs, g, prv, nxt, p, periodic, 20, two=False)
         del state
         if arith == "exact":
             assert np.array_equal(two, one)
