@@ -85,6 +85,24 @@ def test_inprocess_ring_pairs_on_two_gpus(orc, Np):
     assert np.array_equal(res.populations, want)
 
 
+@pytest.mark.parametrize("temporal", ["on", "off"])
+def test_inprocess_ring_of_eight_on_all_gpus(orc, temporal):
+    """An 8-rank 1-D ring (the BASELINE's N=8 decomposition) spread over all
+    visible GPUs (4 here: two ranks per device), peer stores from the step
+    kernels, pairs and single steps: bitwise vs the oracle.  The closest this
+    harness gets to 8 B200s -- every rank talks to its two neighbours only."""
+    vs = tl.build_velocity_set("D2Q37")
+    orc.set_stencil(vs.c, vs.w, vs.cs2)
+    p = tl.PhysicsParams(tau=0.8, gy=-1e-5, Twall_top=0.9 * vs.cs2, Twall_bot=1.1 * vs.cs2)
+    Lx, Ly, steps = 8 * 24, 70, 7
+    res = tl.run(tl.SimConfig(Lx=Lx, Ly=Ly, Np=8, steps=steps, params=p,
+                              init="rayleigh-taylor", exchange="p2p", temporal=temporal,
+                              devices=tuple(range(torch.cuda.device_count()))))
+    f0 = orc.equilibrium(*orc.rayleigh_taylor_macro(Lx, Ly, vs.cs2))
+    want, _ = orc.run(f0, steps, orc.params6(0.8, 0.0, -1e-5, 1.0, p.Twall_top, p.Twall_bot))
+    assert np.array_equal(res.populations, want)
+
+
 @pytest.mark.parametrize("n", [2, 4])
 def test_torchrun_bench_config_pairs(n):
     """configs[2] at N = 2 / 4 (1920x2048 per GPU) under torchrun: exact pairs

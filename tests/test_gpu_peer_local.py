@@ -56,6 +56,7 @@ CASES = [
     # (Np, tiling, Lx, Ly, periodic_y)
     (2, "1d", 2 * 24, 40, False),       # 1-D ring, walls
     (4, "1d", 4 * 16, 36, False),       # 1-D ring of 4, walls
+    (8, "1d", 8 * 12, 36, False),       # 1-D ring of 8
     (2, (1, 2), 40, 2 * 20, True),      # Y split only: X self-periodic, periodic Y ring
     (4, (1, 4), 36, 4 * 12, True),
     (4, (2, 2), 2 * 20, 2 * 18, False),  # 2-D with walls: corners go diagonal
@@ -200,6 +201,7 @@ PAIR_CASES = [
     (2, 2 * 24, 40, True, 9, 0),        # periodic Y, odd: a final single step
     (4, 4 * 20, 130, False, 11, 3),     # 4 ranks, snapshots between pairs
     (3, 3 * 12, 24, False, 6, 0),       # the narrowest tile (12 columns)
+    (8, 8 * 16, 40, False, 6, 0),       # a ring of 8 (the BASELINE's N=8) on one GPU
 ]
 
 
