@@ -897,8 +897,8 @@ static int tb2_setup(tb2::TbLaunch &T, const TlbField *prv, const TlbField *nxt,
     const bool walls = (flags & TLB_F_WALL_BOT) != 0;
     // the first and last strips (wall rows, or the periodic wrap of the
     // level-1 halo rows) are slower per column: they go first, in half runs,
-    // so the schedule does not end on them (periodic C2: 9.0k -> see
-    // profiles/r02_tb2.md)
+    // so the schedule does not end on them (periodic C2: 9.0k -> 13.5k
+    // MLUPS, profiles/r02_tb2.md)
     const bool edges = walls || (flags & TLB_F_WRAP_Y) != 0;
     if (walls && (!(p->Twall_top > 0.0) || !(p->Twall_bot > 0.0)))
         return fail(TLB_ERR_DOMAIN, "equilibrium requires rho > 0 and T > 0");
@@ -924,8 +924,8 @@ static int tb2_setup(tb2::TbLaunch &T, const TlbField *prv, const TlbField *nxt,
     TLB_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     const int hs = tb2_rows(cfg) - 6;     // output rows per strip, at most
     T.ns = (prv->Ly + hs - 1) / hs;
-    // work items: runs of run_l columns of a strip; wall strips (bc rows)
-    // first, in runs of half the length
+    // work items: runs of run_l columns of a strip; the edge strips (wall
+    // rows / periodic wrap) first, in runs of half the length
     const int Lx = prv->Lx;
     T.run_l = tb2_run_length(Lx, T.ns, edges, sms * ((cfg == 1 || cfg >= 7) ? 2 : 1));
     if ((Lx + T.run_l - 1) / T.run_l < min_runs) T.run_l = (Lx + min_runs - 1) / min_runs;
