@@ -761,9 +761,10 @@ class RankWorker:
                 and self._peer is None and not self.debug_poison and self.timing != "every")
 
     # "auto" pairs steps only on tiles this large: the two-step kernel needs
-    # enough strip runs to fill the GPU (1024x2048: 12.7k vs 10.6k MLUPS for
-    # the single step; 256x128: 270 vs 3,200; profiles/r02_tb2.md)
-    PAIR_MIN_SITES = 2_000_000
+    # enough strip runs to fill the GPU (512x1024: 10.3k vs 9.8k MLUPS for
+    # the single step, 1024x1024: 11.0k vs 10.2k, 1024x2048: 12.7k vs 10.6k;
+    # 512x256 and 256x128 lose; profiles/r02_tb2.md)
+    PAIR_MIN_SITES = 500_000
 
     def pairable(self):
         """Two steps per launch (temporal blocking, csrc/tb2.cu): a single
